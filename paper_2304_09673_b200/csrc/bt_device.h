@@ -1,0 +1,124 @@
+// bt_device.h -- kernel argument blocks and launchers (internal to
+// libblobtree_b200.so; the public boundary is include/bt_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt_tile.cuh"
+
+namespace btk {
+
+// Superblock = 8x8 tiles (64x64 pixels): unit of the coarse cone cull.
+constexpr int kSB = 8;
+
+struct DevTree {
+    const float4* words = nullptr;
+    const uint32_t* primWords = nullptr;   // ascending word of each primitive
+    const uint32_t* primOrd = nullptr;     // node ordinal of each primitive
+    const uint32_t* nodeWord = nullptr;    // word of each node ordinal
+    const int32_t* compactAnc = nullptr;   // nearest strict compact ancestor ordinal, -1 none
+    const uint32_t* fullProgram = nullptr; // post-order (isPrim<<31 | op<<26 | word)
+    uint32_t nwords = 0, nnodes = 0, nprims = 0;
+    uint32_t fullDepth = 0;                // max stack depth of a full post-order walk
+};
+
+struct FrameBufs {
+    // camera products
+    float4* rays = nullptr;      // [tiles*64] dir.xyz, dot(dir, forward); tile-major
+    float4* cones = nullptr;     // [tiles] axis.xyz, cos
+    float* coneSin = nullptr;    // [tiles]
+    float4* sbCones = nullptr;   // [superblocks] axis.xyz, half-angle (rad, conservative)
+    // A-buffer
+    uint2* pairs = nullptr;      // (voi, superblock)
+    uint4* pool = nullptr;       // (tile, voi, entry bits, exit bits), unsorted
+    uint4* unsorted = nullptr;   // CSR slots: (word, entry, exit, voi)
+    Frag* frags = nullptr;       // CSR slots, sorted by (zEntry, word)
+    uint32_t* tileCount = nullptr;
+    uint32_t* tileCursor = nullptr;
+    uint32_t* tileLocal = nullptr;   // exclusive scan inside a 4096-tile block
+    uint32_t* blockSum = nullptr;    // per scan block
+    uint32_t* blockPrefix = nullptr; // exclusive over scan blocks (+ total at [nblocks])
+    uint32_t* offsets = nullptr;     // CSR [tiles+1]
+    uint32_t* counters = nullptr;    // see kCnt*
+    uint64_t pairCap = 0, poolCap = 0;
+};
+
+// device counters (uint32 slots)
+enum : int {
+    kCntPairs = 0,
+    kCntPool = 1,
+    kCntScanDone = 2,
+    kCntCandidates = 3,
+    kCntFallback = 4,
+    kCntOverflow = 5,
+    kCntSlots = 8
+};
+
+// device statistics (uint64 slots)
+enum : int {
+    kStFieldEvals = 0,
+    kStRetained,
+    kStPrimEvals,
+    kStFlops,
+    kStMaxOverlap,
+    kStMaxCache,
+    kStTileErrors,
+    kStFallbacks,
+    kStSlots
+};
+
+struct GBuf {
+    uint8_t* hit = nullptr;
+    float* depth = nullptr;
+    float* normal = nullptr;  // xyz interleaved
+    uint32_t* evalCount = nullptr;
+    uint32_t* tileMaxOverlap = nullptr;
+    uint32_t* tileCacheBytes = nullptr;
+    uint8_t* tileError = nullptr;
+    uint32_t* fallback = nullptr;  // pixel indices needing the gradient normal
+    int width = 0, height = 0, tilesX = 0, tilesY = 0;
+};
+
+inline Cam make_cam(const float* pos, const float* fwd, const float* right, const float* up,
+                    float tanHalf, float aspect, float invNear, float invDepthRange, float nearZ,
+                    float farZ, int w, int h) {
+    Cam c;
+    c.pos = F3{pos[0], pos[1], pos[2]};
+    c.fwd = F3{fwd[0], fwd[1], fwd[2]};
+    c.right = F3{right[0], right[1], right[2]};
+    c.up = F3{up[0], up[1], up[2]};
+    c.tanHalf = tanHalf;
+    c.aspect = aspect;
+    c.invNear = invNear;
+    c.invDepthRange = invDepthRange;
+    c.nearZ = nearZ;
+    c.farZ = farZ;
+    c.width = w;
+    c.height = h;
+    return c;
+}
+
+// ---- launchers (k_frame.cu) -------------------------------------------
+void launch_params_update(cudaStream_t st, float4* words, const uint32_t* dWords,
+                          const float* dParams, const uint32_t* dCounts, uint32_t n,
+                          uint32_t stride);
+void launch_roi_all(cudaStream_t st, const DevTree& t, float* roi);
+void launch_voi(cudaStream_t st, const DevTree& t, const float* roi, float margin, Voi* vois);
+void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY);
+void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
+                    const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
+                    int smCount);
+void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
+
+// ---- launchers (k_trace.cu) -------------------------------------------
+void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
+                  uint32_t tile0, uint32_t tile1);
+void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                    const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
+                    uint64_t* stats, int smCount);
+void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                   const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats);
+
+}  // namespace btk

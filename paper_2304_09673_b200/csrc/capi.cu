@@ -1,0 +1,918 @@
+// capi.cu -- context management and the extern "C" boundary (include/bt_cuda.h).
+//
+// A bt_ctx owns every device buffer of the path and one CUDA stream:
+//   tree      : the reference's 16-byte word array, uploaded bit for bit,
+//               plus structure-only side tables (primitive ordinals, the
+//               compact-ancestor chain for ROI, the post-order program).
+//   (a)       : per-node ROI and per-primitive VOIs (64 B each).
+//   (b)       : rays / cones (camera products), candidate pairs, fragment
+//               pool, CSR offsets and the sorted fragment array.
+//   (c)       : the G-buffer planes and device statistics.
+// Buffers are sized lazily and grown on demand; a per-frame CUDA graph is
+// re-captured whenever a buffer moves or the frame key changes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bt_cuda.h"
+#include "bt_device.h"
+
+using namespace btk;
+
+namespace {
+
+thread_local std::string g_lastError;
+
+int fail(int code, const std::string& msg) {
+    g_lastError = msg;
+    return code;
+}
+
+#define BT_CUDA(call)                                                                    \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(e_ == cudaErrorMemoryAllocation ? BT_ENOMEM : BT_ECUDA,          \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+template <class T> struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t reserve(size_t n) {
+        if (n <= cap && ptr) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 1);
+        cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+};
+
+struct FrameKey {
+    bt_camera cam;
+    bt_render_config cfg;
+    uint32_t tile0, tile1;
+    int exact;
+    uint64_t bufEpoch;
+    bool operator==(const FrameKey& o) const { return std::memcmp(this, &o, sizeof(FrameKey)) == 0; }
+};
+
+}  // namespace
+
+struct bt_ctx {
+    int device = 0;
+    int smCount = 148;
+    int smClockKHz = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+
+    // tree
+    DevBuf<float4> words;
+    DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram;
+    DevBuf<int32_t> compactAnc;
+    DevBuf<float> roi;
+    DevBuf<Voi> vois;
+    uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
+    bool haveTree = false;
+    bool haveRoi = false;
+
+    // parameter staging
+    DevBuf<uint32_t> pWords, pCounts;
+    DevBuf<float> pParams;
+
+    // frame
+    int width = 0, height = 0, tilesX = 0, tilesY = 0;
+    DevBuf<float4> rays, cones, sbCones;
+    DevBuf<float> coneSin;
+    DevBuf<uint2> pairs;
+    DevBuf<uint4> pool, unsorted;
+    DevBuf<Frag> frags;
+    DevBuf<uint32_t> tileCount, tileCursor, tileLocal, blockSum, blockPrefix, offsets, counters;
+    bool haveAbuffer = false;
+    bool haveRays = false;
+    bt_camera rayCam{};
+
+    // G-buffer
+    DevBuf<uint8_t> hit, tileError;
+    DevBuf<float> depth, normal;
+    DevBuf<uint32_t> evalCount, tileMaxOverlap, tileCacheBytes, fallback;
+    bool haveGbuffer = false;
+
+    DevBuf<uint64_t> stats;
+
+    uint64_t bufEpoch = 1;
+    cudaGraphExec_t graph = nullptr;
+    FrameKey graphKey{};
+    bool haveGraph = false;
+
+    // profiling (CUDA events around each stage)
+    bool profiling = false;
+    float profMs[4] = {0, 0, 0, 0};
+    uint32_t profLaunch[4] = {0, 0, 0, 0};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+DevTree dev_tree(const bt_ctx* c) {
+    DevTree t;
+    t.words = c->words.ptr;
+    t.primWords = c->primWords.ptr;
+    t.primOrd = c->primOrd.ptr;
+    t.nodeWord = c->nodeWord.ptr;
+    t.compactAnc = c->compactAnc.ptr;
+    t.fullProgram = c->fullProgram.ptr;
+    t.nwords = c->nwords;
+    t.nnodes = c->nnodes;
+    t.nprims = c->nprims;
+    t.fullDepth = c->fullDepth;
+    return t;
+}
+
+FrameBufs frame_bufs(const bt_ctx* c) {
+    FrameBufs f;
+    f.rays = c->rays.ptr;
+    f.cones = c->cones.ptr;
+    f.coneSin = c->coneSin.ptr;
+    f.sbCones = c->sbCones.ptr;
+    f.pairs = c->pairs.ptr;
+    f.pool = c->pool.ptr;
+    f.unsorted = c->unsorted.ptr;
+    f.frags = c->frags.ptr;
+    f.tileCount = c->tileCount.ptr;
+    f.tileCursor = c->tileCursor.ptr;
+    f.tileLocal = c->tileLocal.ptr;
+    f.blockSum = c->blockSum.ptr;
+    f.blockPrefix = c->blockPrefix.ptr;
+    f.offsets = c->offsets.ptr;
+    f.counters = c->counters.ptr;
+    f.pairCap = c->pairs.cap;
+    f.poolCap = c->pool.cap;
+    return f;
+}
+
+GBuf gbuf(const bt_ctx* c) {
+    GBuf g;
+    g.hit = c->hit.ptr;
+    g.depth = c->depth.ptr;
+    g.normal = c->normal.ptr;
+    g.evalCount = c->evalCount.ptr;
+    g.tileMaxOverlap = c->tileMaxOverlap.ptr;
+    g.tileCacheBytes = c->tileCacheBytes.ptr;
+    g.tileError = c->tileError.ptr;
+    g.fallback = c->fallback.ptr;
+    g.width = c->width;
+    g.height = c->height;
+    g.tilesX = c->tilesX;
+    g.tilesY = c->tilesY;
+    return g;
+}
+
+Cam to_cam(const bt_camera& k) {
+    return make_cam(k.position, k.forward, k.right, k.up, k.tanHalf, k.aspect, k.invNear,
+                    k.invDepthRange, k.nearZ, k.farZ, k.width, k.height);
+}
+
+int check_camera(const bt_camera* cam) {
+    if (!cam) return fail(BT_EINVAL, "camera is null");
+    if (cam->width <= 0 || cam->height <= 0) return fail(BT_EINVAL, "camera image size must be positive");
+    return BT_OK;
+}
+
+// (Re)size every per-image buffer for a camera.
+int ensure_image(bt_ctx* c, const bt_camera& cam) {
+    const int tx = (cam.width + kTile - 1) / kTile, ty = (cam.height + kTile - 1) / kTile;
+    if (tx == c->tilesX && ty == c->tilesY && cam.width == c->width && cam.height == c->height) return BT_OK;
+    c->width = cam.width;
+    c->height = cam.height;
+    c->tilesX = tx;
+    c->tilesY = ty;
+    const size_t tiles = (size_t)tx * ty;
+    const size_t px = (size_t)cam.width * cam.height;
+    const size_t nsb = (size_t)((tx + kSB - 1) / kSB) * ((ty + kSB - 1) / kSB);
+    const size_t nscan = (tiles + 4095) / 4096;
+    BT_CUDA(c->rays.reserve(tiles * 64));
+    BT_CUDA(c->cones.reserve(tiles));
+    BT_CUDA(c->coneSin.reserve(tiles));
+    BT_CUDA(c->sbCones.reserve(nsb));
+    BT_CUDA(c->tileCount.reserve(tiles));
+    BT_CUDA(c->tileCursor.reserve(tiles));
+    BT_CUDA(c->tileLocal.reserve(tiles));
+    BT_CUDA(c->blockSum.reserve(nscan));
+    BT_CUDA(c->blockPrefix.reserve(nscan + 1));
+    BT_CUDA(c->offsets.reserve(tiles + 1));
+    BT_CUDA(c->hit.reserve(px));
+    BT_CUDA(c->depth.reserve(px));
+    BT_CUDA(c->normal.reserve(px * 3));
+    BT_CUDA(c->evalCount.reserve(px));
+    BT_CUDA(c->fallback.reserve(px));
+    BT_CUDA(c->tileMaxOverlap.reserve(tiles));
+    BT_CUDA(c->tileCacheBytes.reserve(tiles));
+    BT_CUDA(c->tileError.reserve(tiles));
+    c->haveAbuffer = false;
+    c->haveRays = false;
+    c->haveGbuffer = false;
+    c->bufEpoch++;
+    return BT_OK;
+}
+
+int ensure_frame_caps(bt_ctx* c, size_t pairCap, size_t poolCap) {
+    bool moved = false;
+    if (pairCap > c->pairs.cap) {
+        BT_CUDA(c->pairs.reserve(pairCap));
+        moved = true;
+    }
+    if (poolCap > c->pool.cap) {
+        BT_CUDA(c->pool.reserve(poolCap));
+        BT_CUDA(c->unsorted.reserve(poolCap));
+        BT_CUDA(c->frags.reserve(poolCap));
+        moved = true;
+    }
+    if (moved) c->bufEpoch++;
+    return BT_OK;
+}
+
+void prof_begin(bt_ctx* c) {
+    if (c->profiling) cudaEventRecord(c->ev[0], c->stream);
+}
+void prof_end(bt_ctx* c, int slot) {
+    if (!c->profiling) return;
+    cudaEventRecord(c->ev[1], c->stream);
+    cudaEventSynchronize(c->ev[1]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->profMs[slot] += ms;
+    c->profLaunch[slot] += 1;
+}
+
+TraceParams trace_params(const bt_render_config& cfg, const bt_camera& cam) {
+    TraceParams tp;
+    tp.L = cfg.lipschitz;
+    tp.invL = 1.0f / cfg.lipschitz;
+    tp.relax = cfg.relax;
+    tp.minStep = cfg.minStep;
+    tp.hitEps = cfg.hitEpsilon;
+    tp.maxOverlap = cfg.maxOverlap;
+    tp.maxNew = cfg.maxNewPerFetch;
+    float window = cfg.fetchWindow;
+    if (!(window > 0.0f)) window = (cam.farZ - cam.nearZ) / 20.0f;
+    tp.window = window;
+    return tp;
+}
+
+int check_config(const bt_render_config* cfg) {
+    if (!cfg) return fail(BT_EINVAL, "render config is null");
+    if (!(cfg->relax >= 1.0f && cfg->relax < 2.0f)) return fail(BT_EINVAL, "relaxation factor must lie in [1, 2)");
+    if (!(cfg->lipschitz >= 1.0f)) return fail(BT_EINVAL, "lipschitz bound must be at least 1");
+    if (!(cfg->minStep > 0.0f)) return fail(BT_EINVAL, "min step must be > 0");
+    if (!(cfg->hitEpsilon > 0.0f)) return fail(BT_EINVAL, "hit epsilon must be > 0");
+    if (cfg->maxOverlap == 0 || cfg->maxOverlap > BT_MAX_OVERLAP) return fail(BT_EINVAL, "max overlap must lie in [1, 96]");
+    return BT_OK;
+}
+
+int do_camera(bt_ctx* c, const bt_camera& cam) {
+    int rc = ensure_image(c, cam);
+    if (rc) return rc;
+    launch_camera(c->stream, to_cam(cam), frame_bufs(c), c->tilesX, c->tilesY);
+    c->haveRays = true;
+    c->rayCam = cam;
+    return BT_OK;
+}
+
+int resolve_tiles(bt_ctx* c, uint32_t& tile0, uint32_t& tile1) {
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    if (tile1 == 0 || tile1 > tiles) tile1 = tiles;
+    if (tile0 > tile1) return fail(BT_EINVAL, "tile range is empty or inverted");
+    return BT_OK;
+}
+
+// Launch the A-buffer kernels; in `checked` mode verify the capacities
+// afterwards (one D2H of the counters) and rebuild after growing.
+int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, bool checked) {
+    if (c->pairs.cap == 0) {
+        int rc = ensure_frame_caps(c, std::max<size_t>(1u << 18, (size_t)c->nvoi * 16), 1u << 20);
+        if (rc) return rc;
+    }
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        launch_abuffer(c->stream, to_cam(cam), c->vois.ptr, c->nvoi, frame_bufs(c), c->tilesX, c->tilesY,
+                       tile0, tile1, c->smCount);
+        if (!checked) break;
+        uint32_t cnt[kCntSlots];
+        BT_CUDA(cudaMemcpyAsync(cnt, c->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        const bool pairOver = cnt[kCntPairs] > c->pairs.cap;
+        const bool poolOver = cnt[kCntPool] > c->pool.cap;
+        if (!pairOver && !poolOver) break;
+        int rc = ensure_frame_caps(c, pairOver ? (size_t)cnt[kCntPairs] * 2 : c->pairs.cap,
+                                   poolOver ? (size_t)cnt[kCntPool] * 2 : c->pool.cap);
+        if (rc) return rc;
+    }
+    c->haveAbuffer = true;
+    return BT_OK;
+}
+
+int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
+             int exact) {
+    launch_trace(c->stream, exact != 0, dev_tree(c), to_cam(cam), trace_params(cfg, cam), frame_bufs(c), gbuf(c),
+                 c->stats.ptr, tile0, tile1);
+    c->haveGbuffer = true;
+    return BT_OK;
+}
+
+int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
+    if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
+    launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
+                   c->counters.ptr, c->stats.ptr, c->smCount);
+    return BT_OK;
+}
+
+}  // namespace
+
+// ======================================================================== C-ABI
+
+extern "C" {
+
+const char* bt_last_error(void) { return g_lastError.c_str(); }
+
+int bt_ctx_create(int device, bt_ctx** out) {
+    if (!out) return fail(BT_EINVAL, "out is null");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(BT_ECUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(BT_EINVAL, "device index out of range");
+    BT_CUDA(cudaSetDevice(device));
+    bt_ctx* c = new bt_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->smCount, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&c->smClockKHz, cudaDevAttrClockRate, device);
+    e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(BT_ECUDA, cudaGetErrorString(e));
+    }
+    c->stream = c->own;
+    cudaEventCreate(&c->ev[0]);
+    cudaEventCreate(&c->ev[1]);
+    if (c->stats.reserve(kStSlots) != cudaSuccess || c->counters.reserve(kCntSlots) != cudaSuccess) {
+        delete c;
+        return fail(BT_ENOMEM, "cannot allocate statistics");
+    }
+    cudaMemset(c->stats.ptr, 0, kStSlots * sizeof(uint64_t));
+    cudaMemset(c->counters.ptr, 0, kCntSlots * sizeof(uint32_t));
+    *out = c;
+    return BT_OK;
+}
+
+int bt_ctx_destroy(bt_ctx* c) {
+    if (!c) return BT_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->pWords, &c->pCounts,
+                    &c->tileCount, &c->tileCursor, &c->tileLocal, &c->blockSum, &c->blockPrefix, &c->offsets,
+                    &c->counters, &c->evalCount, &c->tileMaxOverlap, &c->tileCacheBytes, &c->fallback})
+        b->release();
+    c->words.release();
+    c->compactAnc.release();
+    c->roi.release();
+    c->vois.release();
+    c->pParams.release();
+    c->rays.release();
+    c->cones.release();
+    c->sbCones.release();
+    c->coneSin.release();
+    c->pairs.release();
+    c->pool.release();
+    c->unsorted.release();
+    c->frags.release();
+    c->hit.release();
+    c->tileError.release();
+    c->depth.release();
+    c->normal.release();
+    c->stats.release();
+    cudaEventDestroy(c->ev[0]);
+    cudaEventDestroy(c->ev[1]);
+    cudaStreamDestroy(c->own);
+    delete c;
+    return BT_OK;
+}
+
+int bt_sync(bt_ctx* c) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    BT_CUDA(cudaGetLastError());
+    return BT_OK;
+}
+
+int bt_set_stream(bt_ctx* c, void* s) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    c->stream = s ? (cudaStream_t)s : c->own;
+    c->haveGraph = false;
+    return BT_OK;
+}
+
+int bt_device_info(bt_ctx* c, int* sm, int* clk) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (sm) *sm = c->smCount;
+    if (clk) *clk = c->smClockKHz;
+    return BT_OK;
+}
+
+int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node* nodes, uint32_t nnodes,
+                   const uint32_t* primitiveWords, uint32_t nprims, uint32_t rootWord) {
+    if (!c || !data || !nodes || !primitiveWords) return fail(BT_EINVAL, "null tree buffer");
+    if (nwords == 0 || nnodes == 0 || nprims == 0) return fail(BT_EINVAL, "empty tree");
+    if (nwords >= BT_ANCESTOR_SENTINEL) return fail(BT_EINVAL, "tree exceeds the 23-bit node index space");
+    (void)rootWord;
+    // structure-only side tables
+    std::vector<uint32_t> nodeWord(nnodes), primOrd(nprims), program(nnodes);
+    std::vector<int32_t> parentOrd(nnodes, -1), compactAnc(nnodes, -1);
+    for (uint32_t i = 0; i < nnodes; ++i) {
+        nodeWord[i] = nodes[i].word;
+        if (nodes[i].word >= nwords) return fail(BT_EINVAL, "node word out of range");
+        program[i] = ((uint32_t)(nodes[i].isPrimitive ? 1u : 0u) << 31) | ((uint32_t)(nodes[i].nodeOp & 0x1F) << 26) |
+                     (nodes[i].word & BT_ANCESTOR_SENTINEL);
+        if (!nodes[i].isPrimitive) {
+            const int32_t l = nodes[i].leftChild, r = nodes[i].rightChild;
+            if (l < 0 || r < 0 || (uint32_t)l >= nnodes || (uint32_t)r >= nnodes)
+                return fail(BT_EINVAL, "operator child ordinal out of range");
+            parentOrd[l] = (int32_t)i;
+            parentOrd[r] = (int32_t)i;
+        }
+    }
+    // compact ancestor chain: nodes are post-order, parents after children,
+    // so a reverse sweep sees every parent first.
+    for (int64_t i = (int64_t)nnodes - 1; i >= 0; --i) {
+        const int32_t p = parentOrd[i];
+        if (p < 0) continue;
+        const uint8_t op = nodes[p].nodeOp;
+        compactAnc[i] = (op >= 9 && op <= 11) ? p : compactAnc[p];
+    }
+    // map primitive words to ordinals (both ascending)
+    {
+        uint32_t k = 0;
+        for (uint32_t i = 0; i < nnodes && k < nprims; ++i)
+            if (nodes[i].isPrimitive && nodes[i].word == primitiveWords[k]) primOrd[k++] = i;
+        if (k != nprims) return fail(BT_EINVAL, "primitiveWords do not match the node records");
+    }
+    // full post-order stack depth
+    uint32_t depth = 0, maxd = 0;
+    for (uint32_t i = 0; i < nnodes; ++i) {
+        if (nodes[i].isPrimitive) {
+            ++depth;
+        } else {
+            if (depth < 2) return fail(BT_EINVAL, "node records are not a post-order binary tree");
+            --depth;
+        }
+        maxd = std::max(maxd, depth);
+    }
+    BT_CUDA(cudaSetDevice(c->device));
+    BT_CUDA(c->words.reserve(nwords + 8));
+    BT_CUDA(c->primWords.reserve(nprims));
+    BT_CUDA(c->primOrd.reserve(nprims));
+    BT_CUDA(c->nodeWord.reserve(nnodes));
+    BT_CUDA(c->compactAnc.reserve(nnodes));
+    BT_CUDA(c->fullProgram.reserve(nnodes));
+    BT_CUDA(c->roi.reserve(nnodes));
+    BT_CUDA(c->vois.reserve(nprims));
+    BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->primWords.ptr, primitiveWords, nprims * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->primOrd.ptr, primOrd.data(), nprims * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->nodeWord.ptr, nodeWord.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->compactAnc.ptr, compactAnc.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->fullProgram.ptr, program.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    c->nwords = nwords;
+    c->nnodes = nnodes;
+    c->nprims = nprims;
+    c->nvoi = 0;
+    c->fullDepth = maxd;
+    c->haveTree = true;
+    c->haveRoi = false;
+    c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_tree_download(bt_ctx* c, float* data, uint32_t nwords) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (nwords > c->nwords) return fail(BT_EINVAL, "nwords exceeds the uploaded tree");
+    BT_CUDA(cudaMemcpyAsync(data, c->words.ptr, (size_t)nwords * 16, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    return BT_OK;
+}
+
+int bt_params_update_device(bt_ctx* c, const uint32_t* dw, const float* dp, const uint32_t* dc, uint32_t n,
+                            uint32_t stride) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (n == 0) return BT_OK;
+    launch_params_update(c->stream, c->words.ptr, dw, dp, dc, n, stride);
+    return BT_OK;
+}
+
+int bt_params_update(bt_ctx* c, const uint32_t* words, const float* params, const uint32_t* counts, uint32_t n,
+                     uint32_t stride) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (n == 0) return BT_OK;
+    if (!words || !params || !counts) return fail(BT_EINVAL, "null parameter buffer");
+    for (uint32_t i = 0; i < n; ++i) {
+        if (words[i] + 1 + (counts[i] + 3) / 4 > c->nwords || counts[i] > stride)
+            return fail(BT_EINVAL, "parameter update outside the tree");
+    }
+    const bool moved = n > c->pWords.cap || (size_t)n * stride > c->pParams.cap;
+    BT_CUDA(c->pWords.reserve(n));
+    BT_CUDA(c->pCounts.reserve(n));
+    BT_CUDA(c->pParams.reserve((size_t)n * stride));
+    if (moved) c->bufEpoch++;
+    BT_CUDA(cudaMemcpyAsync(c->pWords.ptr, words, n * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->pCounts.ptr, counts, n * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->pParams.ptr, params, (size_t)n * stride * 4, cudaMemcpyHostToDevice, c->stream));
+    launch_params_update(c->stream, c->words.ptr, c->pWords.ptr, c->pParams.ptr, c->pCounts.ptr, n, stride);
+    return BT_OK;
+}
+
+int bt_roi(bt_ctx* c, float* out, uint32_t nnodes) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    prof_begin(c);
+    launch_roi_all(c->stream, dev_tree(c), c->roi.ptr);
+    prof_end(c, 0);
+    c->haveRoi = true;
+    if (out) {
+        if (nnodes != c->nnodes) return fail(BT_EINVAL, "roi output size must equal the node count");
+        BT_CUDA(cudaMemcpyAsync(out, c->roi.ptr, nnodes * 4, cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return BT_OK;
+}
+
+int bt_roi_upload(bt_ctx* c, const float* roi, uint32_t nnodes) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (!roi || nnodes != c->nnodes) return fail(BT_EINVAL, "roi must hold one value per node ordinal");
+    BT_CUDA(cudaMemcpyAsync(c->roi.ptr, roi, nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    c->haveRoi = true;
+    return BT_OK;
+}
+
+int bt_voi_build(bt_ctx* c, float margin) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (!c->haveRoi) return fail(BT_ESTATE, "no range of interest computed or uploaded");
+    prof_begin(c);
+    launch_voi(c->stream, dev_tree(c), c->roi.ptr, margin, c->vois.ptr);
+    prof_end(c, 0);
+    c->nvoi = c->nprims;
+    return BT_OK;
+}
+
+int bt_voi_upload(bt_ctx* c, const bt_voi* v, uint32_t n) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (n && !v) return fail(BT_EINVAL, "null volume buffer");
+    std::vector<Voi> h(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        Voi& d = h[i];
+        d.family = v[i].family;
+        if (d.family > 2u) return fail(BT_EINVAL, "unknown volume family");
+        d.word = v[i].primitiveWord;
+        d.center = F3{v[i].center[0], v[i].center[1], v[i].center[2]};
+        d.radius = v[i].radius;
+        d.half = F3{v[i].halfExtents[0], v[i].halfExtents[1], v[i].halfExtents[2]};
+        d.rot = Q4{v[i].rotation[0], v[i].rotation[1], v[i].rotation[2], v[i].rotation[3]};
+        d.axisEnd = F3{v[i].axisEnd[0], v[i].axisEnd[1], v[i].axisEnd[2]};
+    }
+    if (n > c->vois.cap) {
+        BT_CUDA(c->vois.reserve(n));
+        c->bufEpoch++;
+    }
+    if (n) BT_CUDA(cudaMemcpyAsync(c->vois.ptr, h.data(), n * sizeof(Voi), cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    c->nvoi = n;
+    return BT_OK;
+}
+
+int bt_voi_download(bt_ctx* c, bt_voi* out, uint32_t n) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (n > c->nvoi) return fail(BT_EINVAL, "more volumes requested than built");
+    std::vector<Voi> h(n);
+    if (n) BT_CUDA(cudaMemcpyAsync(h.data(), c->vois.ptr, n * sizeof(Voi), cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    for (uint32_t i = 0; i < n; ++i) {
+        std::memset(&out[i], 0, sizeof(bt_voi));
+        out[i].family = (uint8_t)h[i].family;
+        out[i].primitiveWord = h[i].word;
+        out[i].center[0] = h[i].center.x;
+        out[i].center[1] = h[i].center.y;
+        out[i].center[2] = h[i].center.z;
+        out[i].radius = h[i].radius;
+        out[i].halfExtents[0] = h[i].half.x;
+        out[i].halfExtents[1] = h[i].half.y;
+        out[i].halfExtents[2] = h[i].half.z;
+        out[i].rotation[0] = h[i].rot.w;
+        out[i].rotation[1] = h[i].rot.x;
+        out[i].rotation[2] = h[i].rot.y;
+        out[i].rotation[3] = h[i].rot.z;
+        out[i].axisEnd[0] = h[i].axisEnd.x;
+        out[i].axisEnd[1] = h[i].axisEnd.y;
+        out[i].axisEnd[2] = h[i].axisEnd.z;
+    }
+    return BT_OK;
+}
+
+int bt_abuffer_build(bt_ctx* c, const bt_camera* cam, uint32_t tile0, uint32_t tile1) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    prof_begin(c);
+    rc = do_camera(c, *cam);
+    if (rc) return rc;
+    rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    rc = do_abuffer(c, *cam, tile0, tile1, true);
+    prof_end(c, 1);
+    return rc;
+}
+
+int bt_abuffer_info(bt_ctx* c, uint64_t* fragments, int32_t* tilesX, int32_t* tilesY) {
+    if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    uint32_t total = 0;
+    BT_CUDA(cudaMemcpyAsync(&total, c->offsets.ptr + tiles, 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    if (fragments) *fragments = total;
+    if (tilesX) *tilesX = c->tilesX;
+    if (tilesY) *tilesY = c->tilesY;
+    return BT_OK;
+}
+
+int bt_abuffer_download(bt_ctx* c, uint32_t* offsets, bt_fragment* frags, uint64_t capacity) {
+    if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    std::vector<uint32_t> off(tiles + 1);
+    BT_CUDA(cudaMemcpyAsync(off.data(), c->offsets.ptr, (tiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    if (offsets) std::memcpy(offsets, off.data(), (tiles + 1) * 4);
+    if (frags) {
+        if (capacity < off[tiles]) return fail(BT_EINVAL, "fragment capacity too small");
+        static_assert(sizeof(bt_fragment) == sizeof(Frag), "fragment layout");
+        if (off[tiles])
+            BT_CUDA(cudaMemcpyAsync(frags, c->frags.ptr, (size_t)off[tiles] * sizeof(Frag), cudaMemcpyDeviceToHost,
+                                    c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return BT_OK;
+}
+
+int bt_abuffer_upload(bt_ctx* c, const bt_camera* cam, const uint32_t* offsets, const bt_fragment* frags) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    if (!offsets) return fail(BT_EINVAL, "null offsets");
+    rc = do_camera(c, *cam);
+    if (rc) return rc;
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    const uint32_t total = offsets[tiles];
+    if (total && !frags) return fail(BT_EINVAL, "null fragments");
+    for (uint32_t i = 0; i < tiles; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(BT_EINVAL, "offsets must be non-decreasing");
+    rc = ensure_frame_caps(c, std::max<size_t>(c->pairs.cap, 1u << 16), std::max<size_t>(total, 1u << 16));
+    if (rc) return rc;
+    BT_CUDA(cudaMemcpyAsync(c->offsets.ptr, offsets, (tiles + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    if (total)
+        BT_CUDA(cudaMemcpyAsync(c->frags.ptr, frags, (size_t)total * sizeof(Frag), cudaMemcpyHostToDevice, c->stream));
+    launch_offsets_from_counts(c->stream, frame_bufs(c), tiles);
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    c->haveAbuffer = true;
+    return BT_OK;
+}
+
+int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
+             int exact) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    rc = check_config(cfg);
+    if (rc) return rc;
+    if (!c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
+    if (cam->width != c->width || cam->height != c->height)
+        return fail(BT_EINVAL, "camera image size differs from the A-buffer's");
+    if (!c->haveRays || std::memcmp(&c->rayCam, cam, sizeof(bt_camera)) != 0) {
+        rc = do_camera(c, *cam);
+        if (rc) return rc;
+    }
+    rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    prof_begin(c);
+    rc = do_trace(c, *cam, *cfg, tile0, tile1, exact);
+    prof_end(c, 2);
+    return rc;
+}
+
+int bt_normals(bt_ctx* c, const bt_camera* cam, int mode, int exact) {
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    if (mode != 0 && mode != 1) return fail(BT_EINVAL, "unknown normals mode");
+    prof_begin(c);
+    rc = do_normals(c, *cam, mode, exact);
+    prof_end(c, 3);
+    return rc;
+}
+
+int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, int exact) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    rc = check_config(cfg);
+    if (rc) return rc;
+    if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
+    rc = do_camera(c, *cam);
+    if (rc) return rc;
+    launch_oracle(c->stream, exact != 0, dev_tree(c), to_cam(*cam), trace_params(*cfg, *cam), frame_bufs(c), gbuf(c),
+                  c->stats.ptr);
+    BT_CUDA(cudaMemsetAsync(c->tileMaxOverlap.ptr, 0, c->tileMaxOverlap.cap * 4, c->stream));
+    BT_CUDA(cudaMemsetAsync(c->tileCacheBytes.ptr, 0, c->tileCacheBytes.cap * 4, c->stream));
+    BT_CUDA(cudaMemsetAsync(c->tileError.ptr, 0, c->tileError.cap, c->stream));
+    c->haveGbuffer = true;
+    return BT_OK;
+}
+
+int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
+                    int exact, int use_graph) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    rc = check_config(cfg);
+    if (rc) return rc;
+    rc = ensure_image(c, *cam);
+    if (rc) return rc;
+    rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
+    const int mode = cfg->normalsMode;
+    auto enqueue = [&](bool checked) -> int {
+        launch_roi_all(c->stream, dev_tree(c), c->roi.ptr);
+        launch_voi(c->stream, dev_tree(c), c->roi.ptr, cfg->hitEpsilon, c->vois.ptr);
+        c->haveRoi = true;
+        c->nvoi = c->nprims;
+        int r = do_camera(c, *cam);
+        if (r) return r;
+        r = do_abuffer(c, *cam, tile0, tile1, checked);
+        if (r) return r;
+        r = do_trace(c, *cam, *cfg, tile0, tile1, exact);
+        if (r) return r;
+        return do_normals(c, *cam, mode, exact);
+    };
+    if (!use_graph) return enqueue(true);
+
+    FrameKey key;
+    std::memset(&key, 0, sizeof(key));
+    key.cam = *cam;
+    key.cfg = *cfg;
+    key.tile0 = tile0;
+    key.tile1 = tile1;
+    key.exact = exact;
+    key.bufEpoch = c->bufEpoch;
+    if (!c->haveGraph || !(key == c->graphKey)) {
+        // eager, capacity-checked frame first (grows buffers), then capture
+        rc = enqueue(true);
+        if (rc) return rc;
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        key.bufEpoch = c->bufEpoch;
+        if (c->graph) {
+            cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        BT_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue(false);
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(BT_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&c->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return fail(BT_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        c->graphKey = key;
+        c->haveGraph = true;
+        return BT_OK;  // the eager frame already produced this frame's output
+    }
+    BT_CUDA(cudaGraphLaunch(c->graph, c->stream));
+    return BT_OK;
+}
+
+int bt_gbuffer_download(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
+                        uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
+    cudaStream_t s = c->stream;
+    if (hit) BT_CUDA(cudaMemcpyAsync(hit, c->hit.ptr, px, cudaMemcpyDeviceToHost, s));
+    if (depth) BT_CUDA(cudaMemcpyAsync(depth, c->depth.ptr, px * 4, cudaMemcpyDeviceToHost, s));
+    if (normal) BT_CUDA(cudaMemcpyAsync(normal, c->normal.ptr, px * 12, cudaMemcpyDeviceToHost, s));
+    if (evalCount) BT_CUDA(cudaMemcpyAsync(evalCount, c->evalCount.ptr, px * 4, cudaMemcpyDeviceToHost, s));
+    if (tileMaxOverlap)
+        BT_CUDA(cudaMemcpyAsync(tileMaxOverlap, c->tileMaxOverlap.ptr, tiles * 4, cudaMemcpyDeviceToHost, s));
+    if (tileCacheBytes)
+        BT_CUDA(cudaMemcpyAsync(tileCacheBytes, c->tileCacheBytes.ptr, tiles * 4, cudaMemcpyDeviceToHost, s));
+    if (tileError) BT_CUDA(cudaMemcpyAsync(tileError, c->tileError.ptr, tiles, cudaMemcpyDeviceToHost, s));
+    BT_CUDA(cudaStreamSynchronize(s));
+    BT_CUDA(cudaGetLastError());
+    return BT_OK;
+}
+
+int bt_gbuffer_device(bt_ctx* c, bt_gbuffer_view* out) {
+    if (!c || !out) return fail(BT_EINVAL, "null argument");
+    out->hit = c->hit.ptr;
+    out->depth = c->depth.ptr;
+    out->normal = c->normal.ptr;
+    out->evalCount = c->evalCount.ptr;
+    out->tileMaxOverlap = c->tileMaxOverlap.ptr;
+    out->tileCacheBytes = c->tileCacheBytes.ptr;
+    out->tileError = c->tileError.ptr;
+    out->width = c->width;
+    out->height = c->height;
+    out->tilesX = c->tilesX;
+    out->tilesY = c->tilesY;
+    return BT_OK;
+}
+
+int bt_gbuffer_upload(bt_ctx* c, const bt_camera* cam, const uint8_t* hit, const float* depth) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    if (!hit || !depth) return fail(BT_EINVAL, "null G-buffer plane");
+    rc = do_camera(c, *cam);
+    if (rc) return rc;
+    const size_t px = (size_t)c->width * c->height;
+    BT_CUDA(cudaMemcpyAsync(c->hit.ptr, hit, px, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->depth.ptr, depth, px * 4, cudaMemcpyHostToDevice, c->stream));
+    c->haveGbuffer = true;
+    return BT_OK;
+}
+
+int bt_stats_download(bt_ctx* c, bt_stats* out) {
+    if (!c || !out) return fail(BT_EINVAL, "null argument");
+    uint64_t st[kStSlots];
+    uint32_t cnt[kCntSlots];
+    BT_CUDA(cudaMemcpyAsync(st, c->stats.ptr, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaMemcpyAsync(cnt, c->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    std::memset(out, 0, sizeof(*out));
+    out->fieldEvals = st[kStFieldEvals];
+    out->retainedNodeVisits = st[kStRetained];
+    out->primitiveEvals = st[kStPrimEvals];
+    out->treeNodeCount = c->nnodes;
+    out->maxOverlap = (uint32_t)st[kStMaxOverlap];
+    out->maxCacheBytes = (uint32_t)st[kStMaxCache];
+    out->fieldFlops = st[kStFlops];
+    out->candidatePairs = cnt[kCntCandidates];
+    out->tileErrors = st[kStTileErrors];
+    out->normalFallbacks = st[kStFallbacks];
+    if (c->haveAbuffer) {
+        const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+        uint32_t total = 0;
+        BT_CUDA(cudaMemcpyAsync(&total, c->offsets.ptr + tiles, 4, cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        out->fragments = total;
+    }
+    if (cnt[kCntOverflow] || cnt[kCntPairs] > c->pairs.cap)
+        return fail(BT_ENOMEM, "A-buffer capacity overflowed during a graph replay; re-run eagerly");
+    return BT_OK;
+}
+
+int bt_stats_reset(bt_ctx* c) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    BT_CUDA(cudaMemsetAsync(c->stats.ptr, 0, kStSlots * sizeof(uint64_t), c->stream));
+    return BT_OK;
+}
+
+int bt_profile_enable(bt_ctx* c, int on) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    c->profiling = on != 0;
+    for (int i = 0; i < 4; ++i) {
+        c->profMs[i] = 0.f;
+        c->profLaunch[i] = 0;
+    }
+    return BT_OK;
+}
+
+int bt_profile_read(bt_ctx* c, float* ms4, uint32_t* l4) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    for (int i = 0; i < 4; ++i) {
+        if (ms4) ms4[i] = c->profMs[i];
+        if (l4) l4[i] = c->profLaunch[i];
+    }
+    return BT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,452 @@
+// k_frame.cu -- stages (a) and (b) on sm_100a.
+//
+//   k_params_update  per-frame primitive parameter rewrite      (linear_tree.cpp:187-193)
+//   k_roi_all        range of interest per node                 (linear_tree.cpp:170-185)
+//   k_voi            volume of interest per primitive           (linear_tree.cpp:216-283)
+//   k_camera         pixel rays, tile cones, superblock cones   (camera.cpp:29-37, abuffer.cpp:117-149)
+//   k_pairs          (volume, superblock) coarse cull           (superset of abuffer.cpp:193-196)
+//   k_raster         exact tile cull + 64 pixel-ray intervals   (abuffer.cpp:188-222)
+//   k_scan           tile counts -> CSR offsets (single pass)
+//   k_scatter        unsorted pool -> CSR slots
+//   k_sort           per-tile rank sort by (zEntry, word)       (insert_sorted, abuffer.cpp:166-173)
+//
+// Everything on the A-buffer path is evaluated with ExactOps (no FMA, IEEE
+// div/sqrt), so (tile, word) membership and (zEntry, zExit) are bit-exact
+// with the reference's single-threaded rasterize_volumes.
+#include "bt_device.h"
+
+namespace btk {
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kScanBlock = 4096;  // tiles per scan block (1024 threads x 4)
+
+// ---------------------------------------------------------------- (a)
+
+__global__ void k_params_update(float4* words, const uint32_t* dWords, const float* dParams,
+                                const uint32_t* dCounts, uint32_t n, uint32_t stride) {
+    const uint32_t i = blockIdx.x * blockDim.y + threadIdx.y;
+    if (i >= n) return;
+    const uint32_t w = dWords[i];
+    const uint32_t cnt = dCounts[i];
+    float* dst = reinterpret_cast<float*>(words + w + 1);
+    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) dst[k] = dParams[(size_t)i * stride + k];
+}
+
+// roi(n) = max(0, d of every compact strict ancestor): the top-down
+// max-propagation of propagate_roi, unrolled along the compact-ancestor chain.
+__device__ __forceinline__ float roi_of(const DevTree& t, uint32_t ord) {
+    float r = 0.0f;
+    int32_t a = t.compactAnc[ord];
+    while (a >= 0) {
+        const float d = __ldg(&t.words[t.nodeWord[a] + 1].y);
+        r = smax(r, d);
+        a = t.compactAnc[a];
+    }
+    return r;
+}
+
+__global__ void k_roi_all(DevTree t, float* roi) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < t.nnodes) roi[i] = roi_of(t, i);
+}
+
+__global__ void k_voi(DevTree t, const float* roi, float margin, Voi* vois) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= t.nprims) return;
+    const uint32_t w = t.primWords[i];
+    const uint32_t blob = __float_as_uint(__ldg(&t.words[w].x));
+    float P[20];
+    const float4* src = t.words + w + 1;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        float4 q = __ldg(&src[k]);
+        P[4 * k] = q.x;
+        P[4 * k + 1] = q.y;
+        P[4 * k + 2] = q.z;
+        P[4 * k + 3] = q.w;
+    }
+    vois[i] = make_voi(blob_op(blob), w, P, roi[t.primOrd[i]], margin);
+}
+
+// ---------------------------------------------------------------- camera
+
+// One CTA per superblock: 4096 rays, 64 tile cones, 1 conservative
+// superblock cone containing all of its tile cones.
+__global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY) {
+    __shared__ float4 sCone[64];
+    __shared__ float sSin[64];
+    __shared__ int sValid[64];
+    const int sbX = (tilesX + kSB - 1) / kSB;
+    const int sx = blockIdx.x % sbX, sy = blockIdx.x / sbX;
+    for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
+        const int lt = k >> 6, pix = k & 63;
+        const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
+        if (tx >= tilesX || ty >= tilesY) continue;
+        const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
+        if (px >= cam.width || py >= cam.height) continue;
+        const RayDir r = pixel_ray(cam, px, py);
+        fb.rays[(size_t)(ty * tilesX + tx) * 64 + pix] = make_float4(r.dir.x, r.dir.y, r.dir.z, r.ddf);
+    }
+    if (threadIdx.x < 64) {
+        const int lt = threadIdx.x;
+        const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
+        const bool valid = tx < tilesX && ty < tilesY;
+        sValid[lt] = valid;
+        if (valid) {
+            const Cone c = tile_cone(cam, tx, ty);
+            const float4 v = make_float4(c.axis.x, c.axis.y, c.axis.z, c.cosH);
+            fb.cones[ty * tilesX + tx] = v;
+            fb.coneSin[ty * tilesX + tx] = c.sinH;
+            sCone[lt] = v;
+            sSin[lt] = c.sinH;
+        }
+    }
+    __syncthreads();
+    // superblock cone: axis = normalized sum of tile axes, half-angle =
+    // max over tiles of angle(axis, tile axis) + tile half-angle, padded.
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        float ax = 0.f, ay = 0.f, az = 0.f;
+        for (int lt = l; lt < 64; lt += 32)
+            if (sValid[lt]) {
+                ax += sCone[lt].x;
+                ay += sCone[lt].y;
+                az += sCone[lt].z;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            ax += __shfl_xor_sync(kFull, ax, o);
+            ay += __shfl_xor_sync(kFull, ay, o);
+            az += __shfl_xor_sync(kFull, az, o);
+        }
+        const float inv = rsqrtf(ax * ax + ay * ay + az * az);
+        ax *= inv;
+        ay *= inv;
+        az *= inv;
+        float th = 0.f;
+        for (int lt = l; lt < 64; lt += 32)
+            if (sValid[lt]) {
+                const float4 c = sCone[lt];
+                const float cx = ay * c.z - az * c.y, cy = az * c.x - ax * c.z, cz = ax * c.y - ay * c.x;
+                const float sn = sqrtf(cx * cx + cy * cy + cz * cz);
+                const float cs = ax * c.x + ay * c.y + az * c.z;
+                const float ang = atan2f(sn, cs) + atan2f(sSin[lt], c.w);
+                th = fmaxf(th, ang);
+            }
+        for (int o = 16; o > 0; o >>= 1) th = fmaxf(th, __shfl_xor_sync(kFull, th, o));
+        if (l == 0) {
+            // absolute + relative padding: float rounding of the exact tile
+            // test is ~1e-6 relative, the pad is two orders above it.
+            th = th * 1.0001f + 2e-4f;
+            fb.sbCones[blockIdx.x] = make_float4(ax, ay, az, th);
+        }
+    }
+}
+
+// Conservative superblock test: true whenever cone_may_touch would be true
+// for at least one of its tiles ("coarse cull").
+__device__ __forceinline__ bool sb_may_touch(float4 sc, F3 apex, const Sphere& s) {
+    const float th = sc.w;
+    if (th >= 1.5f) return true;
+    const float vx = s.c.x - apex.x, vy = s.c.y - apex.y, vz = s.c.z - apex.z;
+    const float d2 = vx * vx + vy * vy + vz * vz;
+    const float len = sqrtf(d2);
+    const float pad = 1e-4f * len + 1e-5f * fabsf(s.r) + 1e-6f;
+    if (len <= s.r + pad) return true;
+    const float x = vx * sc.x + vy * sc.y + vz * sc.z;
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    if (x < len * sn + pad) return true;  // wrap-around region behind the cone
+    const float y = sqrtf(fmaxf(d2 - x * x, 0.0f));
+    return cs * y - sn * x <= s.r + pad;
+}
+
+// one warp per volume: near/far cull (abuffer.cpp:188-191), then the
+// coarse superblock cull; surviving (volume, superblock) pairs are appended.
+__global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_t nvoi, FrameBufs fb,
+                                                int tilesX, int tilesY, uint32_t tile0,
+                                                uint32_t tile1) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nvoi) return;
+    const Voi v = vois[warp];
+    const Sphere bs = bounding_sphere(v);
+    const float vz = view_z(cam, bs.c);
+    if (E::add(vz, bs.r) < cam.nearZ || E::sub(vz, bs.r) > cam.farZ) return;
+    const int sbX = (tilesX + kSB - 1) / kSB, sbY = (tilesY + kSB - 1) / kSB;
+    const int nsb = sbX * sbY;
+    for (int base = 0; base < nsb; base += 32) {
+        const int sb = base + lane;
+        bool pass = false;
+        if (sb < nsb) {
+            const int sx = sb % sbX, sy = sb / sbX;
+            const uint32_t first = (uint32_t)(sy * kSB * tilesX + sx * kSB);
+            const int lastTy = min(sy * kSB + kSB, tilesY) - 1, lastTx = min(sx * kSB + kSB, tilesX) - 1;
+            const uint32_t last = (uint32_t)(lastTy * tilesX + lastTx);
+            if (last >= tile0 && first < tile1) pass = sb_may_touch(fb.sbCones[sb], cam.pos, bs);
+        }
+        const uint32_t m = __ballot_sync(kFull, pass);
+        if (m == 0u) continue;
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(&fb.counters[kCntPairs], (uint32_t)__popc(m));
+        slot = __shfl_sync(kFull, slot, 0) + __popc(m & ((1u << lane) - 1u));
+        if (pass && slot < fb.pairCap) fb.pairs[slot] = make_uint2(warp, (uint32_t)sb);
+    }
+}
+
+// one warp per (volume, superblock) pair, grid-stride.  Lanes test the 64
+// tiles' exact cones, then every surviving tile is swept by the warp: two
+// pixel rays per lane, exact interval + clip + NDC, warp min/max.
+__global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameBufs fb, int tilesX,
+                                                 int tilesY, uint32_t tile0, uint32_t tile1) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t npairs = min((uint64_t)fb.counters[kCntPairs], fb.pairCap);
+    const int sbX = (tilesX + kSB - 1) / kSB;
+    for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npairs; p += nwarps) {
+        const uint2 pr = fb.pairs[p];
+        const Voi v = vois[pr.x];
+        const Sphere bs = bounding_sphere(v);
+        const int sx = pr.y % sbX, sy = pr.y / sbX;
+        bool pass[2];
+        uint32_t tiles[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int lt = lane + 32 * h;
+            const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
+            pass[h] = false;
+            tiles[h] = (uint32_t)(ty * tilesX + tx);
+            if (tx < tilesX && ty < tilesY && tiles[h] >= tile0 && tiles[h] < tile1) {
+                const float4 c = fb.cones[tiles[h]];
+                Cone k;
+                k.axis = F3{c.x, c.y, c.z};
+                k.cosH = c.w;
+                k.sinH = fb.coneSin[tiles[h]];
+                pass[h] = cone_may_touch(k, cam.pos, bs);
+            }
+        }
+        uint64_t mask = (uint64_t)__ballot_sync(kFull, pass[0]) | ((uint64_t)__ballot_sync(kFull, pass[1]) << 32);
+        if (mask == 0) continue;
+        if (lane == 0) atomicAdd(&fb.counters[kCntCandidates], (uint32_t)__popcll(mask));
+        // per-volume constants shared by every ray
+        F3 ol{0.f, 0.f, 0.f};
+        if (v.family == 1u) ol = qrotate<E>(qconj(v.rot), vsub<E>(cam.pos, v.center));
+        while (mask) {
+            const int lt = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
+            const uint32_t tile = (uint32_t)(ty * tilesX + tx);
+            float entry = f_inf(), exitv = -f_inf();
+            bool any = false;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int pix = lane + 32 * h;
+                const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
+                if (px >= cam.width || py >= cam.height) continue;
+                const float4 rd = fb.rays[(size_t)tile * 64 + pix];
+                const F3 d{rd.x, rd.y, rd.z};
+                float t0, t1;
+                bool hit;
+                if (v.family == 0u)
+                    hit = ray_sphere(cam.pos, d, v.center, v.radius, t0, t1);
+                else if (v.family == 1u)
+                    hit = ray_obb_local(ol, d, v.rot, v.half, t0, t1);
+                else
+                    hit = ray_capsule(cam.pos, d, v.center, v.axisEnd, v.radius, t0, t1);
+                if (!hit) continue;
+                float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
+                if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
+                vz0 = smax(vz0, cam.nearZ);
+                vz1 = smin(vz1, cam.farZ);
+                entry = smin(entry, ndc_from_view_z(cam, vz0));
+                exitv = smax(exitv, ndc_from_view_z(cam, vz1));
+                any = true;
+            }
+            if (!__any_sync(kFull, any)) continue;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
+                exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
+            }
+            if (lane == 0) {
+                const uint32_t slot = atomicAdd(&fb.counters[kCntPool], 1u);
+                if (slot < fb.poolCap)
+                    fb.pool[slot] = make_uint4(tile, pr.x, __float_as_uint(entry), __float_as_uint(exitv));
+                else
+                    atomicExch(&fb.counters[kCntOverflow], 1u);
+                atomicAdd(&fb.tileCount[tile], 1u);
+            }
+        }
+    }
+}
+
+// Single-pass scan: every 1024-thread block scans 4096 tile counts locally
+// and publishes its sum; the last block to finish scans the block sums.
+// offset(tile) = tileLocal[tile] + blockPrefix[tile / 4096].
+__global__ void __launch_bounds__(1024) k_scan(FrameBufs fb, uint32_t tiles) {
+    __shared__ uint32_t warpSums[32];
+    __shared__ bool amLast;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t base = blockIdx.x * kScanBlock + tid * 4;
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = (base + k < tiles) ? fb.tileCount[base + k] : 0u;
+    const uint32_t local = v[0] + v[1] + v[2] + v[3];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += n;
+    }
+    if (lane == 31) warpSums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t s = warpSums[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(kFull, s, o);
+            if (lane >= o) s += n;
+        }
+        warpSums[lane] = s;  // inclusive
+    }
+    __syncthreads();
+    uint32_t run = incl - local + (wid > 0 ? warpSums[wid - 1] : 0u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (base + k < tiles) fb.tileLocal[base + k] = run;
+        run += v[k];
+    }
+    if (tid == 0) {
+        fb.blockSum[blockIdx.x] = warpSums[31];
+        __threadfence();
+        const uint32_t done = atomicAdd(&fb.counters[kCntScanDone], 1u);
+        amLast = (done == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (amLast && wid == 0) {
+        __threadfence();
+        uint32_t carry = 0;
+        for (uint32_t b0 = 0; b0 < gridDim.x; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const uint32_t s = b < gridDim.x ? *((volatile uint32_t*)&fb.blockSum[b]) : 0u;
+            uint32_t inc = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t n = __shfl_up_sync(kFull, inc, o);
+                if (lane >= o) inc += n;
+            }
+            if (b < gridDim.x) fb.blockPrefix[b] = carry + inc - s;
+            carry += __shfl_sync(kFull, inc, 31);
+        }
+        if (lane == 0) fb.blockPrefix[gridDim.x] = carry;
+    }
+}
+
+__device__ __forceinline__ uint32_t tile_offset(const FrameBufs& fb, uint32_t tile) {
+    return fb.tileLocal[tile] + fb.blockPrefix[tile / kScanBlock];
+}
+
+__global__ void k_scatter(const Voi* vois, FrameBufs fb) {
+    const uint32_t n = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint4 r = fb.pool[i];
+        const uint32_t slot = tile_offset(fb, r.x) + atomicAdd(&fb.tileCursor[r.x], 1u);
+        fb.unsorted[slot] = make_uint4(vois[r.y].word, r.z, r.w, r.y);
+    }
+}
+
+// key order of insert_sorted: (zEntry, word); equal keys keep volume order
+// (upper_bound insertion in volume order), hence the volume index tiebreak.
+__device__ __forceinline__ bool key_less(const uint4& a, const uint4& b) {
+    const float ea = __uint_as_float(a.y), eb = __uint_as_float(b.y);
+    if (ea != eb) return ea < eb;
+    if (a.x != b.x) return a.x < b.x;
+    return a.w < b.w;
+}
+
+constexpr int kSortStage = 256;
+
+__global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles) {
+    __shared__ uint4 stage[4][kSortStage];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x * 4 + wid;
+    if (tile >= tiles) return;
+    const uint32_t n = fb.tileCount[tile];
+    const uint32_t off = tile_offset(fb, tile);
+    fb.offsets[tile] = off;
+    if (tile == tiles - 1 && lane == 0) fb.offsets[tiles] = off + n;
+    if (n == 0) return;
+    const uint4* src = fb.unsorted + off;
+    const bool staged = n <= (uint32_t)kSortStage;
+    if (staged)
+        for (uint32_t i = lane; i < n; i += 32) stage[wid][i] = src[i];
+    __syncwarp();
+    const uint4* keys = staged ? stage[wid] : src;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint4 me = keys[i];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < n; ++j) rank += key_less(keys[j], me) ? 1u : 0u;
+        Frag f;
+        f.word = me.x;
+        f.zEntry = __uint_as_float(me.y);
+        f.zExit = __uint_as_float(me.z);
+        fb.frags[off + rank] = f;
+    }
+}
+
+__global__ void k_offsets_from_counts(FrameBufs fb, uint32_t tiles) {
+    // used when the A-buffer was uploaded: counts from CSR offsets
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < tiles) fb.tileCount[i] = fb.offsets[i + 1] - fb.offsets[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+
+void launch_params_update(cudaStream_t st, float4* words, const uint32_t* dWords,
+                          const float* dParams, const uint32_t* dCounts, uint32_t n,
+                          uint32_t stride) {
+    if (n == 0) return;
+    dim3 block(32, 8);
+    k_params_update<<<(n + 7) / 8, block, 0, st>>>(words, dWords, dParams, dCounts, n, stride);
+}
+
+void launch_roi_all(cudaStream_t st, const DevTree& t, float* roi) {
+    if (t.nnodes == 0) return;
+    k_roi_all<<<(t.nnodes + 255) / 256, 256, 0, st>>>(t, roi);
+}
+
+void launch_voi(cudaStream_t st, const DevTree& t, const float* roi, float margin, Voi* vois) {
+    if (t.nprims == 0) return;
+    k_voi<<<(t.nprims + 127) / 128, 128, 0, st>>>(t, roi, margin, vois);
+}
+
+void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY) {
+    const int nsb = ((tilesX + kSB - 1) / kSB) * ((tilesY + kSB - 1) / kSB);
+    k_camera<<<nsb, 256, 0, st>>>(cam, fb, tilesX, tilesY);
+}
+
+void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
+                    const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
+                    int smCount) {
+    const uint32_t tiles = (uint32_t)(tilesX * tilesY);
+    cudaMemsetAsync(fb.counters, 0, kCntSlots * sizeof(uint32_t), st);
+    cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
+    cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
+    if (nvoi > 0) {
+        k_pairs<<<(nvoi * 32 + 255) / 256, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1);
+        k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
+    }
+    const uint32_t nblocks = (tiles + kScanBlock - 1) / kScanBlock;
+    k_scan<<<nblocks, 1024, 0, st>>>(fb, tiles);
+    k_scatter<<<smCount * 4, 256, 0, st>>>(vois, fb);
+    k_sort<<<(tiles + 3) / 4, 128, 0, st>>>(fb, tiles);
+}
+
+void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles) {
+    k_offsets_from_counts<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
+}
+
+}  // namespace btk

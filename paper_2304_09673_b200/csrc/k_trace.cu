@@ -1,0 +1,403 @@
+// k_trace.cu -- stage (c) on sm_100a: synchronized per-tile sphere tracing,
+// normals, and the GPU brute-force oracle.
+//
+//   k_trace<O>     one warp per 8x8 tile, two pixel rays per lane; lane 0
+//                  runs fetch_interval + view build (tracer.cpp:50-103,
+//                  traversal.cpp:88-99) in shared memory, then all 64 rays
+//                  march in lockstep over the pruned view with warp votes
+//                  retiring finished rays (render_tiles, tracer.cpp:141-236).
+//   k_normals      depth-differential normals (tracer.cpp:296-350); pixels
+//                  without usable neighbours are queued for k_gradient.
+//   k_gradient<O>  one warp per queued pixel, lanes 0..5 each run one full
+//                  post-order tree walk (eval_full, traversal.cpp:126-141).
+//   k_oracle<O>    oracle_render (tracer.cpp:238-280): every pixel marched
+//                  over [near, far] on the full tree.
+//
+// O = ExactOps gives bit-identical results to the CPU reference; O = FastOps
+// lets nvcc contract the field arithmetic into FFMA (tolerance path).
+#include "bt_device.h"
+
+namespace btk {
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kTraceWarps = 4;
+constexpr int kFullStackCap = 128;
+
+template <class O> __device__ __forceinline__ F3 ray_point(F3 o, F3 d, float t) {
+    return vadd<O>(o, vscale<O>(d, t));
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+template <class O>
+__global__ void __launch_bounds__(kTraceWarps * 32) k_trace(DevTree t, Cam cam, TraceParams tp,
+                                                            FrameBufs fb, GBuf g, uint64_t* stats,
+                                                            uint32_t tile0, uint32_t tile1) {
+    extern __shared__ __align__(16) unsigned char smemRaw[];
+    WarpSmem* smem = reinterpret_cast<WarpSmem*>(smemRaw);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& s = smem[wid];
+    const uint32_t tile = tile0 + blockIdx.x * kTraceWarps + wid;
+    if (tile >= tile1) return;
+    const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
+
+    int px[2], py[2];
+    bool valid[2], found[2], hitf[2] = {false, false};
+    float depth[2] = {0.0f, 0.0f};
+    uint32_t evals[2] = {0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int li = lane + 32 * j;
+        px[j] = tx * kTile + (li & 7);
+        py[j] = ty * kTile + (li >> 3);
+        valid[j] = px[j] < g.width && py[j] < g.height;
+        found[j] = !valid[j];
+    }
+    const uint32_t off = fb.offsets[tile];
+    const uint32_t cnt = fb.offsets[tile + 1] - off;
+    const Frag* list = fb.frags + off;
+
+    uint32_t tileMaxOv = 0, tileCache = 0, tileErr = 0;
+    uint64_t stFE = 0, stRNV = 0, stPE = 0, stFL = 0;
+
+    if (cnt != 0) {
+        F3 dir[2];
+        float ddf[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            dir[j] = F3{0.f, 0.f, 1.f};
+            ddf[j] = 1.0f;
+            if (valid[j]) {
+                const float4 r = fb.rays[(size_t)tile * 64 + lane + 32 * j];
+                dir[j] = F3{r.x, r.y, r.z};
+                ddf[j] = r.w;
+            }
+        }
+        for (uint32_t i = lane; i < cnt && i < (uint32_t)kFragStage; i += 32) s.stage[i] = list[i];
+        if (lane == 0) {
+            s.nAct = 0;
+            s.cursor = 0;
+            s.zEnd = 0.0f;
+            s.err = 0;
+        }
+        __syncwarp();
+
+        for (;;) {
+            if (__all_sync(kFull, found[0] && found[1])) break;
+            if (lane == 0) {
+                uint32_t fetched = 0;
+                const bool ok = fetch_interval(s, list, cnt, cam, tp, fetched);
+                s.done = ok ? 0u : 1u;
+                if (ok) build_view(s, t.words);
+            }
+            __syncwarp();
+            if (s.done) break;
+            const uint32_t overlap = s.nAct;
+            tileMaxOv = max(tileMaxOv, overlap);
+            if (s.err) {
+                tileErr = 1;
+                break;
+            }
+            tileCache = max(tileCache, s.cacheFloats * 4u);
+            if (!s.rootUsed) continue;
+            const float zb = s.zBegin, ze = s.zEnd;
+            if (ze <= zb) continue;
+            if (s.maxDepth > kStackCap) {  // eval_pruned would throw on first use
+                tileErr = 1;
+                break;
+            }
+            const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
+            March m[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (!found[j])
+                    march_begin(m[j], E::div(vz0, ddf[j]), E::div(vz1, ddf[j]));
+                else {
+                    m[j].phase = 0;
+                    m[j].evals = 0;
+                    m[j].hit = false;
+                }
+            }
+            // lockstep march: one field evaluation per active ray per step
+            for (;;) {
+                const bool a0 = m[0].phase != 0, a1 = m[1].phase != 0;
+                const uint32_t both = __ballot_sync(kFull, a0 && a1);
+                const uint32_t anyA = __ballot_sync(kFull, a0 || a1);
+                if (anyA == 0u) break;
+                if (both != 0u) {
+                    F3 pts[2] = {ray_point<O>(cam.pos, dir[0], m[0].evalT),
+                                 ray_point<O>(cam.pos, dir[1], m[1].evalT)};
+                    float v[2];
+                    eval_view<O, 2>(s, t.words, pts, v);
+                    if (a0) march_consume(m[0], v[0], tp);
+                    if (a1) march_consume(m[1], v[1], tp);
+                } else {
+                    const int j = a0 ? 0 : 1;
+                    F3 pts[1] = {ray_point<O>(cam.pos, j == 0 ? dir[0] : dir[1],
+                                              j == 0 ? m[0].evalT : m[1].evalT)};
+                    float v[1];
+                    eval_view<O, 1>(s, t.words, pts, v);
+                    if (a0)
+                        march_consume(m[0], v[0], tp);
+                    else if (a1)
+                        march_consume(m[1], v[0], tp);
+                }
+            }
+            const uint32_t nView = s.nView, nPrim = s.nPrim, fl = s.flops;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (found[j]) continue;
+                const uint32_t e = m[j].evals;
+                evals[j] += e;
+                stFE += e;
+                stRNV += (uint64_t)e * nView;
+                stPE += (uint64_t)e * nPrim;
+                stFL += (uint64_t)e * fl;
+                if (m[j].hit) {
+                    found[j] = true;
+                    hitf[j] = true;
+                    depth[j] = m[j].hitT;
+                }
+            }
+            __syncwarp();
+        }
+    }
+
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        if (!valid[j]) continue;
+        const size_t p = (size_t)py[j] * g.width + px[j];
+        g.hit[p] = hitf[j] ? 1 : 0;
+        g.depth[p] = hitf[j] ? depth[j] : 0.0f;
+        g.evalCount[p] = evals[j];
+    }
+    stFE = warp_sum_u64(stFE);
+    stRNV = warp_sum_u64(stRNV);
+    stPE = warp_sum_u64(stPE);
+    stFL = warp_sum_u64(stFL);
+    if (lane == 0) {
+        g.tileMaxOverlap[tile] = tileMaxOv;
+        g.tileCacheBytes[tile] = tileCache;
+        g.tileError[tile] = (uint8_t)tileErr;
+        if (stFE) {
+            atomicAdd((unsigned long long*)&stats[kStFieldEvals], (unsigned long long)stFE);
+            atomicAdd((unsigned long long*)&stats[kStRetained], (unsigned long long)stRNV);
+            atomicAdd((unsigned long long*)&stats[kStPrimEvals], (unsigned long long)stPE);
+            atomicAdd((unsigned long long*)&stats[kStFlops], (unsigned long long)stFL);
+        }
+        if (tileMaxOv) atomicMax((unsigned long long*)&stats[kStMaxOverlap], (unsigned long long)tileMaxOv);
+        if (tileCache) atomicMax((unsigned long long*)&stats[kStMaxCache], (unsigned long long)tileCache);
+        if (tileErr) atomicAdd((unsigned long long*)&stats[kStTileErrors], 1ull);
+    }
+}
+
+// ---------------------------------------------------------------- full tree
+
+template <class O> __device__ float eval_full(const DevTree& t, F3 p) {
+    float stk[kFullStackCap];
+    int sp = 0;
+    for (uint32_t i = 0; i < t.nnodes; ++i) {
+        const uint32_t e = __ldg(&t.fullProgram[i]);
+        const uint32_t w = e & kSentinel;
+        const float4* P4 = t.words + w + 1;
+        if (e >> 31) {
+            float P[20];
+            const uint32_t kind = (e >> 26) & 0x1Fu;
+            load_params<5>(P, P4);
+            stk[sp++] = eval_primitive<O>(kind, P, p);
+        } else {
+            const uint32_t code = (e >> 26) & 0x1Fu;
+            float kd[2] = {0.f, 0.f};
+            if (code >= 6u) {
+                const float4 q = __ldg(P4);
+                kd[0] = q.x;
+                kd[1] = q.y;
+            }
+            const float right = stk[sp - 1], left = stk[sp - 2];
+            stk[sp - 2] = eval_operator<O>(code, kd, left, right);
+            --sp;
+        }
+    }
+    return stk[0];
+}
+
+__device__ __forceinline__ F3 ray_dir_at(const FrameBufs& fb, const GBuf& g, int x, int y) {
+    const uint32_t tile = (uint32_t)((y >> 3) * g.tilesX + (x >> 3));
+    const float4 r = fb.rays[(size_t)tile * 64 + ((y & 7) << 3) + (x & 7)];
+    return F3{r.x, r.y, r.z};
+}
+
+__device__ __forceinline__ F3 position_at(const Cam& cam, const FrameBufs& fb, const GBuf& g, int x, int y) {
+    const F3 d = ray_dir_at(fb, g, x, y);
+    return vadd<E>(cam.pos, vscale<E>(d, g.depth[(size_t)y * g.width + x]));
+}
+
+__global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* counters) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= g.width || y >= g.height) return;
+    const size_t p = (size_t)y * g.width + x;
+    float* nout = g.normal + 3 * p;
+    if (!g.hit[p]) {
+        nout[0] = nout[1] = nout[2] = 0.0f;
+        return;
+    }
+    bool ok = false;
+    F3 n{0.f, 0.f, 0.f};
+    if (mode == 0) {
+        auto hitAt = [&](int xx, int yy) {
+            return xx >= 0 && xx < g.width && yy >= 0 && yy < g.height && g.hit[(size_t)yy * g.width + xx] != 0;
+        };
+        const F3 pc = position_at(cam, fb, g, x, y);
+        const bool l = hitAt(x - 1, y), r = hitAt(x + 1, y), u = hitAt(x, y - 1), d = hitAt(x, y + 1);
+        F3 ddx{0.f, 0.f, 0.f}, ddy{0.f, 0.f, 0.f};
+        bool okX = true, okY = true;
+        if (l && r) ddx = vsub<E>(position_at(cam, fb, g, x + 1, y), position_at(cam, fb, g, x - 1, y));
+        else if (r) ddx = vsub<E>(position_at(cam, fb, g, x + 1, y), pc);
+        else if (l) ddx = vsub<E>(pc, position_at(cam, fb, g, x - 1, y));
+        else okX = false;
+        if (u && d) ddy = vsub<E>(position_at(cam, fb, g, x, y + 1), position_at(cam, fb, g, x, y - 1));
+        else if (d) ddy = vsub<E>(position_at(cam, fb, g, x, y + 1), pc);
+        else if (u) ddy = vsub<E>(pc, position_at(cam, fb, g, x, y - 1));
+        else okY = false;
+        if (okX && okY) {
+            n = vcross<E>(ddx, ddy);
+            const float len = vlen<E>(n);
+            if (len > 1e-12f) {
+                n = vdivs<E>(n, len);
+                if (vdot<E>(n, ray_dir_at(fb, g, x, y)) > 0.0f) n = vneg(n);
+                ok = true;
+            }
+        }
+    }
+    if (ok) {
+        nout[0] = n.x;
+        nout[1] = n.y;
+        nout[2] = n.z;
+    } else {
+        const uint32_t slot = atomicAdd(&counters[kCntFallback], 1u);
+        g.fallback[slot] = (uint32_t)p;
+    }
+}
+
+// gradient_normal (tracer.cpp:285-294): lanes 0..5 evaluate the full tree at
+// p +- h e_axis, h = max(1e-3, 1e-4 t).
+template <class O>
+__global__ void __launch_bounds__(128) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
+                                                  const uint32_t* counters, uint64_t* stats) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n = counters[kCntFallback];
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+        const uint32_t p = g.fallback[i];
+        const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
+        const F3 pc = position_at(cam, fb, g, x, y);
+        const float depth = g.depth[p];
+        const float h = smax(1e-3f, E::mul(1e-4f, depth));
+        float v = 0.0f;
+        if (lane < 6) {
+            F3 q = pc;
+            const int axis = lane >> 1;
+            if (axis == 0) q.x = (lane & 1) ? E::sub(pc.x, h) : E::add(pc.x, h);
+            if (axis == 1) q.y = (lane & 1) ? E::sub(pc.y, h) : E::add(pc.y, h);
+            if (axis == 2) q.z = (lane & 1) ? E::sub(pc.z, h) : E::add(pc.z, h);
+            v = eval_full<O>(t, q);
+        }
+        float f[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) f[k] = __shfl_sync(kFull, v, k);
+        if (lane == 0) {
+            const F3 dv{E::sub(f[0], f[1]), E::sub(f[2], f[3]), E::sub(f[4], f[5])};
+            const F3 nn = vnormalize<E>(dv);
+            g.normal[3 * p + 0] = nn.x;
+            g.normal[3 * p + 1] = nn.y;
+            g.normal[3 * p + 2] = nn.z;
+        }
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
+}
+
+// oracle_render: one thread per pixel over [near, far], full tree.
+template <class O>
+__global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf g, uint64_t* stats) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    uint64_t fe = 0;
+    if (x < g.width && y < g.height) {
+        const size_t p = (size_t)y * g.width + x;
+        const uint32_t tile = (uint32_t)((y >> 3) * g.tilesX + (x >> 3));
+        const float4 r = fb.rays[(size_t)tile * 64 + ((y & 7) << 3) + (x & 7)];
+        const F3 d{r.x, r.y, r.z};
+        March m;
+        march_begin(m, E::div(cam.nearZ, r.w), E::div(cam.farZ, r.w));
+        while (m.phase != 0) {
+            const float v = eval_full<O>(t, ray_point<O>(cam.pos, d, m.evalT));
+            march_consume(m, v, tp);
+        }
+        g.hit[p] = m.hit ? 1 : 0;
+        g.depth[p] = m.hit ? m.hitT : 0.0f;
+        g.evalCount[p] = m.evals;
+        fe = m.evals;
+    }
+    // warp-aggregate the counters
+    const uint64_t s = warp_sum_u64(fe);
+    if ((threadIdx.x + threadIdx.y * blockDim.x) % 32 == 0 && s) {
+        atomicAdd((unsigned long long*)&stats[kStFieldEvals], (unsigned long long)s);
+        atomicAdd((unsigned long long*)&stats[kStRetained], (unsigned long long)(s * t.nnodes));
+        atomicAdd((unsigned long long*)&stats[kStPrimEvals], (unsigned long long)(s * t.nprims));
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+
+void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
+                  uint32_t tile0, uint32_t tile1) {
+    if (tile1 <= tile0) return;
+    const uint32_t n = tile1 - tile0;
+    const size_t smem = sizeof(WarpSmem) * kTraceWarps;
+    const uint32_t blocks = (n + kTraceWarps - 1) / kTraceWarps;
+    static bool attrSet = false;
+    if (!attrSet) {
+        cudaFuncSetAttribute(k_trace<ExactOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_trace<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attrSet = true;
+    }
+    if (exact) {
+        k_trace<ExactOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1);
+    } else {
+        k_trace<FastOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1);
+    }
+}
+
+void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                    const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
+                    uint64_t* stats, int smCount) {
+    cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
+    dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
+    k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
+    if (exact)
+        k_gradient<ExactOps><<<smCount * 4, 128, 0, st>>>(t, cam, fb, g, counters, stats);
+    else
+        k_gradient<FastOps><<<smCount * 4, 128, 0, st>>>(t, cam, fb, g, counters, stats);
+}
+
+void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                   const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats) {
+    dim3 block(16, 8), grid((g.width + 15) / 16, (g.height + 7) / 8);
+    if (exact)
+        k_oracle<ExactOps><<<grid, block, 0, st>>>(t, cam, tp, fb, g, stats);
+    else
+        k_oracle<FastOps><<<grid, block, 0, st>>>(t, cam, tp, fb, g, stats);
+}
+
+}  // namespace btk
