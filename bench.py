@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""bench.py -- synchronized tracing of a 1,000-primitive blobtree at 1080p.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one frame of the reference's per-frame pipeline on the C3 workload
+(SURVEY.md appendix C): per-frame primitive-parameter update (all 1,000
+primitives perturbed) -> (a) ROI + VOIs -> (b) 8x8-tile A-buffer -> (c)
+synchronized sphere tracing -> normals, replayed from one CUDA graph.
+
+* value       Mrays/s = W*H / device time per frame (CUDA events on the
+              stream the kernels run on; L2 flushed between frames by a
+              256 MiB write that is not timed); inputs resident in HBM.
+* e2e         the same through the public C-ABI with HOST buffers: pinned
+              H2D of the frame's parameter deltas and D2H of the whole
+              G-buffer (hit, depth, normal, evalCount, tile planes) per step.
+* roofline    the field-evaluation kernel (k_trace) against the measured FP32
+              (FFMA) peak of the box: algorithmic flops per frame (SURVEY.md
+              appendix B, counted on the device) / the kernel's CUDA-event time.
+* cpu_baseline the unmodified reference (oracle/_ref) timed on this host's
+              cores on one C3 frame.
+--impl reference times that reference CPU path per step instead.
+Multi-GPU (torchrun): the frame's tile rows are split over ranks (strong
+scaling); each rank traces its rows and rank 0 gathers hit/depth/evalCount
+with NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mrays/s and ms/frame at 1080p vs primitive count; % FP32 peak (field eval)"
+WORKLOAD = ("C3: synthetic blobtree, 1,000 primitives (250 compact-union cells x 4, sharp-union comb), "
+            "1920x1080, all primitive parameters perturbed every frame")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--exact", action="store_true", help="IEEE-exact kernels instead of FMA field evaluation")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+def cpu_frame_reference(config: str, frames: int, threads: int):
+    """Time the unmodified reference library (oracle/_ref) on `frames` frames."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bridge import RefScene, ref_available  # CPU checker: bench's CPU legs only
+    from paper_2304_09673_b200.pipeline import RenderConfig
+    if not ref_available():
+        return None
+    cfg = RenderConfig()
+    r = RefScene(config)
+    times, stages = [], []
+    for f in range(frames):
+        r.perturb(f)
+        t0 = time.perf_counter()
+        _, _, ms, _ = r.frame(cfg, threads)
+        times.append(time.perf_counter() - t0)
+        stages.append(ms)
+    return r.width * r.height, times, np.mean(stages, axis=0)
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    out = cpu_frame_reference(args.config, args.warmup + args.steps, threads)
+    if out is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbt_ref.so not built (needs "
+                                                               "/root/reference at build time)"}))
+        return
+    rays, times, stages = out
+    timed = times[args.warmup:]
+    ms = 1e3 * float(np.mean(timed))
+    value = rays / (ms * 1e-3) / 1e6
+    sample = (f"{len(timed)} full {args.config} frames: propagate_roi+build_volumes_of_interest, rasterize_volumes "
+              f"(single-threaded by design), render_tiles ({threads} threads), compute_normals; mean stage ms "
+              f"{[round(float(s), 2) for s in stages]}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD if args.config == "C3" else args.config, "threads": threads},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mrays/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- B200 arm
+
+def run_b200(args, rank: int, world: int, local_rank: int):
+    import ctypes as C
+
+    import torch
+
+    from paper_2304_09673_b200 import _capi as capi
+    from paper_2304_09673_b200.pipeline import RenderConfig, Renderer, Scene
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # a real (non-NULL) stream shared by torch and the library: the events
+    # below record on the stream the kernels actually run on
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    lib = capi.load()
+
+    scene = Scene.build(args.config)
+    rd = Renderer(local_rank)
+    rd.set_stream(stream.cuda_stream)
+    rd.upload(scene)
+    cam = scene.device_camera
+    cfg = RenderConfig()
+    exact = bool(args.exact)
+    W, H = scene.width, scene.height
+    tiles_x, tiles_y = scene.tiles
+    # strong scaling: contiguous tile-row ranges per rank
+    from paper_2304_09673_b200.distributed import tile_row_ranges
+    rows = tile_row_ranges(tiles_y, world)
+    tile0, tile1 = int(rows[rank] * tiles_x), int(rows[rank + 1] * tiles_x)
+    if world == 1:
+        tile0, tile1 = 0, 0
+
+    # all frames' parameter deltas resident in HBM before timing
+    nframes = args.warmup + args.steps
+    host_frames = [scene.perturb(f) for f in range(nframes)]
+    nprim = len(scene.prims)
+    d_words = [torch.from_numpy(w.view(np.int32)).to(dev) for w, _, _ in host_frames]
+    d_params = [torch.from_numpy(p).to(dev) for _, p, _ in host_frames]
+    d_counts = [torch.from_numpy(c.view(np.int32)).to(dev) for _, _, c in host_frames]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes, tile_row_ranges
+    planes = {}
+
+    def step(f):
+        rd.update_params_device(d_words[f].data_ptr(), d_params[f].data_ptr(), d_counts[f].data_ptr(), nprim)
+        rd.render_frame(cam, cfg, exact=exact, graph=True, tile0=tile0, tile1=tile1, normals=(world == 1))
+        if world > 1:
+            # the only exchange: this rank's rows of hit/depth/evalCount -> rank 0,
+            # then normals over the whole image on rank 0 (they need neighbour rows)
+            if not planes:
+                planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
+            gather_rows(planes, rows, rank, world, W, H)
+            if rank == 0:
+                rd.compute_normals(cam, cfg.normalsMode, exact)
+
+    for f in range(args.warmup):
+        step(f)
+    torch.cuda.synchronize(dev)
+
+    # ------------------------------------------------------------------ timed region
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local_rank) as clocks:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step(args.warmup + i)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t_wall = time.perf_counter() - t_wall
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clock = clocks.summary()
+    kernels, nodes = C.c_uint32(), C.c_uint32()
+    capi.check(lib.bt_graph_kernel_count(rd.ctx, C.byref(kernels), C.byref(nodes)), "bt_graph_kernel_count")
+    launches = args.steps * (kernels.value + 1)  # graph kernels + the parameter-update kernel
+    value = W * H / (ms * 1e-3) / 1e6
+
+    if rank != 0:
+        return
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural scene, fixed seed)",
+        "config": {"workload": WORKLOAD if args.config == "C3" else args.config, "primitives": nprim,
+                   "resolution": f"{W}x{H}", "rays_per_frame": W * H,
+                   "field_eval": "ieee-exact" if exact else "fma-contracted (tolerance path)",
+                   "l2": "flushed between timed frames (256 MiB device write, untimed)",
+                   "parallelism": f"tile rows over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "graph": f"{kernels.value} kernels / {nodes.value} nodes per frame"},
+        "gpu_launches": launches,
+        "clocks": {k: clock[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+    }
+
+    # ------------------------------------------------------------------ per-stage + roofline (untimed pass)
+    stage_ms, flops_per_frame, st = stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim)
+    peak = C.c_float()
+    capi.check(lib.bt_fp32_peak(local_rank, C.byref(peak), None), "bt_fp32_peak")
+    trace_ms = stage_ms["trace"]
+    achieved = flops_per_frame / (trace_ms * 1e-3) / 1e12
+    result["stages_ms"] = {k: round(v, 4) for k, v in stage_ms.items()}
+    result["roofline"] = {
+        "kernel": "k_trace (synchronized per-tile sphere tracing + field evaluation)",
+        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak.value, 2), "unit": "TFLOP/s",
+        "frac": round(achieved / peak.value, 4), "traffic": None,
+        "peak_source": "measured FFMA microbenchmark on this box (bt_fp32_peak); MEASURED_PEAKS.json has no FP32 figure",
+        "work": f"{flops_per_frame / 1e9:.3f} GFLOP/frame algorithmic (SURVEY.md appendix B), "
+                f"{st.fieldEvals} field evals/frame",
+    }
+    result["frame_stats"] = {"fieldEvals": st.fieldEvals, "fragments": st.fragments,
+                             "candidatePairs": st.candidatePairs, "maxOverlap": st.maxOverlap,
+                             "normalFallbacks": st.normalFallbacks, "tileErrors": st.tileErrors}
+
+    # ------------------------------------------------------------------ e2e through the C-ABI with host buffers
+    if world == 1:
+        result["e2e"] = e2e_pass(rd, scene, cam, cfg, exact, host_frames, args)
+
+    # ------------------------------------------------------------------ CPU reference beside it
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        out = cpu_frame_reference(args.config, 1, threads)
+        if out is not None:
+            rays, times, stages = out
+            v = rays / times[0] / 1e6
+            result["cpu_baseline"] = {
+                "value": round(v, 3), "unit": "Mrays/s", "cores": threads, "kind": "reference",
+                "sample": f"1 full {args.config} frame through the unmodified reference (oracle/_ref): stage ms "
+                          f"roi+voi {stages[0]:.1f}, rasterize {stages[1]:.1f} (single-threaded by design), "
+                          f"render_tiles {stages[2]:.1f} ({threads} threads), normals {stages[3]:.1f}"}
+    if not args.no_sweep and world == 1:
+        result["sweep_ms_per_frame"] = sweep(rd, exact)
+    print(json.dumps(result), flush=True)
+
+
+def stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim, frames: int = 5):
+    """Eager pass with CUDA events around each stage (bt_profile_*)."""
+    import ctypes as C
+
+    from paper_2304_09673_b200 import _capi as capi
+    lib = rd.lib
+    c = cfg.to_c()
+    rd.profile(True)
+    st = None
+    flops = []
+    for f in range(frames):
+        rd.update_params_device(d_words[f].data_ptr(), d_params[f].data_ptr(), d_counts[f].data_ptr(), nprim)
+        rd.reset_stats()
+        capi.check(lib.bt_roi(rd.ctx, None, 0), "bt_roi")
+        capi.check(lib.bt_voi_build(rd.ctx, C.c_float(cfg.hitEpsilon)), "bt_voi_build")
+        capi.check(lib.bt_abuffer_build(rd.ctx, C.byref(cam), 0, 0), "bt_abuffer_build")
+        capi.check(lib.bt_trace(rd.ctx, C.byref(cam), C.byref(c), 0, 0, int(exact)), "bt_trace")
+        capi.check(lib.bt_normals(rd.ctx, C.byref(cam), cfg.normalsMode, int(exact)), "bt_normals")
+        st = rd.stats()
+        flops.append(st.fieldFlops)
+    ms, n = rd.profile_read()
+    rd.profile(False)
+    names = ["roi_voi", "abuffer", "trace", "normals"]
+    stage = {names[i]: float(ms[i]) / max(int(n[i]), 1) for i in range(4)}
+    stage["roi_voi"] *= 2  # roi and voi are two profiled calls per frame
+    return stage, float(np.mean(flops)), st
+
+
+def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
+    import torch
+    W, H = scene.width, scene.height
+    tx, ty = scene.tiles
+    n = len(scene.prims)
+    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    frames = [(pin(w.view(np.int32)), pin(p), pin(c.view(np.int32))) for w, p, c in host_frames]
+    out = {k: torch.empty(s, dtype=d).pin_memory() for k, s, d in
+           (("hit", W * H, torch.uint8), ("depth", W * H, torch.float32), ("normal", W * H * 3, torch.float32),
+            ("evalCount", W * H, torch.int32), ("tmo", tx * ty, torch.int32), ("tcb", tx * ty, torch.int32),
+            ("terr", tx * ty, torch.uint8))}
+    lib = rd.lib
+    import ctypes as C
+    from paper_2304_09673_b200 import _capi as capi
+
+    def step(f):
+        w, p, c = frames[f]
+        capi.check(lib.bt_params_update(rd.ctx, C.c_void_p(w.data_ptr()), C.c_void_p(p.data_ptr()),
+                                        C.c_void_p(c.data_ptr()), n, 17), "bt_params_update")
+        rd.render_frame(cam, cfg, exact=exact, graph=True)
+        capi.check(lib.bt_gbuffer_download(rd.ctx, *[C.c_void_p(out[k].data_ptr()) for k in
+                                                     ("hit", "depth", "normal", "evalCount", "tmo", "tcb", "terr")]),
+                   "bt_gbuffer_download")
+
+    for f in range(args.warmup):
+        step(f)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = (time.perf_counter() - t0) / args.steps
+    h2d = n * (4 + 17 * 4 + 4)
+    d2h = W * H * (1 + 4 + 12 + 4) + tx * ty * (4 + 4 + 1)
+    return {"value": round(W * H / dt / 1e6, 2), "unit": "Mrays/s", "ms_per_step": round(dt * 1e3, 4),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "bt_params_update (pinned host) -> bt_render_frame -> bt_gbuffer_download (pinned host), wall clock"}
+
+
+def sweep(rd_unused, exact) -> dict:
+    """ms/frame vs primitive count on the other configs (device time, 10 frames)."""
+    import torch
+
+    from paper_2304_09673_b200.pipeline import RenderConfig, Renderer, Scene
+    res = {}
+    cfg = RenderConfig()
+    stream = torch.cuda.current_stream()
+    assert stream.cuda_stream != 0
+    for name in ("C1", "C2", "C5"):
+        s = Scene.build(name)
+        r = Renderer(torch.cuda.current_device())
+        r.set_stream(stream.cuda_stream)
+        r.upload(s)
+        for _ in range(3):
+            r.render_frame(s.device_camera, cfg, exact=exact, graph=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(10):
+            r.render_frame(s.device_camera, cfg, exact=exact, graph=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        res[name] = {"primitives": len(s.prims), "resolution": f"{s.width}x{s.height}", "ms_per_frame": round(ms, 4),
+                     "Mrays_s": round(s.width * s.height / ms / 1e3, 1)}
+        r.close()
+        s.close()
+    return res
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

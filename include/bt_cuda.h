@@ -190,11 +190,17 @@ BT_API int bt_normals(bt_ctx* ctx, const bt_camera* cam, int mode, int exact);
 BT_API int bt_oracle_render(bt_ctx* ctx, const bt_camera* cam, const bt_render_config* cfg,
                             int exact);
 
-/* One whole frame: (a) -> (b) -> (c) -> normals, optionally replayed from a
- * CUDA graph (use_graph != 0; the graph is re-captured when the camera,
- * config or tile range changes). */
+/* One whole frame: (a) -> (b) -> (c) -> normals.  flags: BT_FRAME_GRAPH
+ * replays the frame from a CUDA graph (re-captured when the camera, config,
+ * tile range or a buffer changes); BT_FRAME_NO_NORMALS stops after tracing
+ * (multi-GPU ranks: normals run after the row gather). */
+#define BT_FRAME_GRAPH 1
+#define BT_FRAME_NO_NORMALS 2
 BT_API int bt_render_frame(bt_ctx* ctx, const bt_camera* cam, const bt_render_config* cfg,
-                           uint32_t tile0, uint32_t tile1, int exact, int use_graph);
+                           uint32_t tile0, uint32_t tile1, int exact, int flags);
+
+/* Kernel nodes in the captured per-frame graph (0 before the first capture). */
+BT_API int bt_graph_kernel_count(bt_ctx* ctx, uint32_t* kernels, uint32_t* nodes);
 
 BT_API int bt_gbuffer_download(bt_ctx* ctx, uint8_t* hit, float* depth, float* normal,
                                uint32_t* evalCount, uint32_t* tileMaxOverlap,
@@ -210,6 +216,9 @@ BT_API int bt_stats_reset(bt_ctx* ctx);
  * reset when profiling is enabled: [roi_voi, abuffer, trace, normals]. */
 BT_API int bt_profile_enable(bt_ctx* ctx, int on);
 BT_API int bt_profile_read(bt_ctx* ctx, float* ms4, uint32_t* launches4);
+/* Measured non-tensor FP32 peak of `device` (FFMA microbenchmark, TFLOP/s):
+ * the roofline denominator of the field-evaluation kernel. */
+BT_API int bt_fp32_peak(int device, float* tflops, float* ms);
 
 #ifdef __cplusplus
 }

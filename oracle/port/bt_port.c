@@ -4,9 +4,9 @@
  * Arithmetic is IEEE binary32 one operation at a time in the reference's
  * order (build with -ffp-contract=off); quadric analysis is fp64 with libm.
  */
+#define _GNU_SOURCE
 #include "bt_port.h"
 
-#define _GNU_SOURCE
 #include <math.h>
 #include <pthread.h>
 #include <stdatomic.h>

@@ -117,7 +117,7 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                   uint32_t tile0, uint32_t tile1);
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
-                    uint64_t* stats, int smCount);
+                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps);
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                    const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats);
 

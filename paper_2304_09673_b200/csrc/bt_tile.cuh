@@ -269,53 +269,34 @@ template <int N> BT_DEV void load_params(float* dst, const float4* src) {
     }
 }
 
-template <class O, int NR>
-BT_DEV void eval_prim_node(uint32_t kind, const float4* P4, const F3* pts, float* out) {
-    float P[20];
-    switch (kind) {
-        case 0: load_params<2>(P, P4); break;              // 8 floats
-        case 5: load_params<5>(P, P4); break;              // 17 floats
-        case 2: load_params<3>(P, P4); break;              // 9 floats
-        default: load_params<3>(P, P4); break;             // 10 floats
-    }
-#pragma unroll
-    for (int r = 0; r < NR; ++r) out[r] = eval_primitive<O>(kind, P, pts[r]);
-}
-
-// Evaluates the view at NR points; returns false on stack overflow (never
-// reached when maxDepth <= 22 was checked by the caller).
-template <class O, int NR>
-BT_DEV void eval_view(const WarpSmem& s, const float4* words, const F3* pts, float* out) {
-    float stk[NR][kStackCap];
+// One field value of the view at p (Algorithm 3): primitives push, operators
+// pop two and push one; the per-node parameter block is loaded as float4s.
+template <class O>
+BT_DEV float eval_view(const WarpSmem& s, const float4* words, F3 p) {
+    float stk[kStackCap];
     uint32_t sp = 0;
     const uint32_t n = s.nView;
     for (uint32_t i = 0; i < n; ++i) {
         const uint32_t b = s.vBlob[i];
         const float4* P4 = words + s.vWord[i] + 1;
+        const uint32_t code = blob_op(b);
         if (blob_is_prim(b)) {
-            float v[NR];
-            eval_prim_node<O, NR>(blob_op(b), P4, pts, v);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) stk[r][sp] = v[r];
-            ++sp;
+            float P[20];
+            load_params<5>(P, P4);
+            stk[sp++] = eval_primitive<O>(code, P, p);
         } else {
-            const uint32_t code = blob_op(b);
             float kd[2] = {0.0f, 0.0f};
             if (code >= 6u) {
-                float4 q = __ldg(P4);
+                const float4 q = __ldg(P4);
                 kd[0] = q.x;
                 kd[1] = q.y;
             }
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const float right = stk[r][sp - 1], left = stk[r][sp - 2];
-                stk[r][sp - 2] = eval_operator<O>(code, kd, left, right);
-            }
+            const float right = stk[sp - 1], left = stk[sp - 2];
+            stk[sp - 2] = eval_operator<O>(code, kd, left, right);
             --sp;
         }
     }
-#pragma unroll
-    for (int r = 0; r < NR; ++r) out[r] = stk[r][0];
+    return stk[0];
 }
 
 // --------------------------------------------------------------------------
@@ -386,6 +367,13 @@ BT_DEV void march_advance(March& m, const TraceParams& tp) {
         m.t = tn;
         m.f = fn;
     }
+}
+
+BT_DEV void march_idle(March& m) {
+    m.phase = 0;
+    m.evals = 0;
+    m.hit = false;
+    m.hitT = 0.0f;
 }
 
 BT_DEV void march_begin(March& m, float t0, float t1) {

@@ -111,9 +111,12 @@ struct bt_ctx {
     bool haveGbuffer = false;
 
     DevBuf<uint64_t> stats;
+    DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
+    uint32_t gradWarps = 0;
 
     uint64_t bufEpoch = 1;
     cudaGraphExec_t graph = nullptr;
+    uint32_t graphKernels = 0, graphNodes = 0;
     FrameKey graphKey{};
     bool haveGraph = false;
 
@@ -314,6 +317,12 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
         BT_CUDA(cudaStreamSynchronize(c->stream));
         const bool pairOver = cnt[kCntPairs] > c->pairs.cap;
         const bool poolOver = cnt[kCntPool] > c->pool.cap;
+        // a dropped pair also drops its fragments: grow the pool with it
+        if (pairOver && !poolOver) {
+            int rc = ensure_frame_caps(c, (size_t)cnt[kCntPairs] * 2, c->pool.cap * 2);
+            if (rc) return rc;
+            continue;
+        }
         if (!pairOver && !poolOver) break;
         int rc = ensure_frame_caps(c, pairOver ? (size_t)cnt[kCntPairs] * 2 : c->pairs.cap,
                                    poolOver ? (size_t)cnt[kCntPool] * 2 : c->pool.cap);
@@ -333,8 +342,16 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
 
 int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
     if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
+    if (c->gradWarps == 0) {
+        // up to 4 warps per SM, at most ~256 MiB of scratch for huge trees
+        const size_t per = (size_t)c->nprims * 6;
+        size_t warps = std::min<size_t>((size_t)c->smCount * 4, std::max<size_t>(1, (256u << 20) / (per * 4)));
+        BT_CUDA(c->gradScratch.reserve(warps * per));
+        c->gradWarps = (uint32_t)warps;
+        c->bufEpoch++;
+    }
     launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
-                   c->counters.ptr, c->stats.ptr, c->smCount);
+                   c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps);
     return BT_OK;
 }
 
@@ -404,6 +421,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->depth.release();
     c->normal.release();
     c->stats.release();
+    c->gradScratch.release();
     cudaEventDestroy(c->ev[0]);
     cudaEventDestroy(c->ev[1]);
     cudaStreamDestroy(c->own);
@@ -502,6 +520,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     c->nprims = nprims;
     c->nvoi = 0;
     c->fullDepth = maxd;
+    c->gradWarps = 0;  // re-sized for the new primitive count on first use
     c->haveTree = true;
     c->haveRoi = false;
     c->bufEpoch++;
@@ -749,7 +768,9 @@ int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cf
 }
 
 int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
-                    int exact, int use_graph) {
+                    int exact, int flags) {
+    const bool use_graph = (flags & BT_FRAME_GRAPH) != 0;
+    const bool normals = (flags & BT_FRAME_NO_NORMALS) == 0;
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -772,7 +793,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         if (r) return r;
         r = do_trace(c, *cam, *cfg, tile0, tile1, exact);
         if (r) return r;
-        return do_normals(c, *cam, mode, exact);
+        return normals ? do_normals(c, *cam, mode, exact) : BT_OK;
     };
     if (!use_graph) return enqueue(true);
 
@@ -782,7 +803,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
     key.cfg = *cfg;
     key.tile0 = tile0;
     key.tile1 = tile1;
-    key.exact = exact;
+    key.exact = exact | (normals ? 0 : 2);
     key.bufEpoch = c->bufEpoch;
     if (!c->haveGraph || !(key == c->graphKey)) {
         // eager, capacity-checked frame first (grows buffers), then capture
@@ -800,6 +821,20 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(BT_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        {
+            size_t nn = 0;
+            cudaGraphGetNodes(g, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            cudaGraphGetNodes(g, nodes.data(), &nn);
+            uint32_t kernels = 0;
+            for (auto& n : nodes) {
+                cudaGraphNodeType ty;
+                cudaGraphNodeGetType(n, &ty);
+                if (ty == cudaGraphNodeTypeKernel) ++kernels;
+            }
+            c->graphKernels = kernels;
+            c->graphNodes = (uint32_t)nn;
+        }
         ce = cudaGraphInstantiate(&c->graph, g, 0);
         cudaGraphDestroy(g);
         if (ce != cudaSuccess) return fail(BT_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
@@ -808,6 +843,13 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         return BT_OK;  // the eager frame already produced this frame's output
     }
     BT_CUDA(cudaGraphLaunch(c->graph, c->stream));
+    return BT_OK;
+}
+
+int bt_graph_kernel_count(bt_ctx* c, uint32_t* kernels, uint32_t* nodes) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (kernels) *kernels = c->haveGraph ? c->graphKernels : 0;
+    if (nodes) *nodes = c->haveGraph ? c->graphNodes : 0;
     return BT_OK;
 }
 

@@ -139,7 +139,7 @@ void Renderer::render(const CameraFrame& frame, const RenderConfig& cfg, bool ex
     flush_params();
     const bt_camera cam = to_device_camera(frame);
     const bt_render_config dc = to_device_config(cfg);
-    check_device(bt_render_frame(ctx_, &cam, &dc, 0, 0, exact ? 1 : 0, useGraph ? 1 : 0), "bt_render_frame");
+    check_device(bt_render_frame(ctx_, &cam, &dc, 0, 0, exact ? 1 : 0, useGraph ? BT_FRAME_GRAPH : 0), "bt_render_frame");
 }
 
 GBuffer Renderer::download() const {

@@ -347,7 +347,14 @@ __device__ __forceinline__ uint32_t tile_offset(const FrameBufs& fb, uint32_t ti
     return fb.tileLocal[tile] + fb.blockPrefix[tile / kScanBlock];
 }
 
+// true when this frame's fragments do not fit the pool (the host grows the
+// buffers and rebuilds; in a graph replay the A-buffer degrades to empty)
+__device__ __forceinline__ bool pool_overflowed(const FrameBufs& fb) {
+    return (uint64_t)fb.counters[kCntPool] > fb.poolCap || (uint64_t)fb.counters[kCntPairs] > fb.pairCap;
+}
+
 __global__ void k_scatter(const Voi* vois, FrameBufs fb) {
+    if (pool_overflowed(fb)) return;
     const uint32_t n = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint4 r = fb.pool[i];
@@ -372,6 +379,14 @@ __global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tile = blockIdx.x * 4 + wid;
     if (tile >= tiles) return;
+    if (pool_overflowed(fb)) {  // never index past the pool: empty A-buffer, flagged
+        if (lane == 0) {
+            fb.offsets[tile] = 0;
+            if (tile == tiles - 1) fb.offsets[tiles] = 0;
+            if (tile == 0) atomicExch(&fb.counters[kCntOverflow], 1u);
+        }
+        return;
+    }
     const uint32_t n = fb.tileCount[tile];
     const uint32_t off = tile_offset(fb, tile);
     fb.offsets[tile] = off;

@@ -29,6 +29,18 @@ template <class O> __device__ __forceinline__ F3 ray_point(F3 o, F3 d, float t) 
     return vadd<O>(o, vscale<O>(d, t));
 }
 
+struct RayLane {
+    March m;
+    F3 dir;
+    uint32_t slot;
+};
+
+__device__ __forceinline__ void swap_lanes(RayLane& a, RayLane& b) {
+    const RayLane t = a;
+    a = b;
+    b = t;
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -36,7 +48,7 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 
 template <class O>
-__global__ void __launch_bounds__(kTraceWarps * 32) k_trace(DevTree t, Cam cam, TraceParams tp,
+__global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam cam, TraceParams tp,
                                                             FrameBufs fb, GBuf g, uint64_t* stats,
                                                             uint32_t tile0, uint32_t tile1) {
     extern __shared__ __align__(16) unsigned char smemRaw[];
@@ -113,56 +125,45 @@ __global__ void __launch_bounds__(kTraceWarps * 32) k_trace(DevTree t, Cam cam, 
                 break;
             }
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
-            March m[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                if (!found[j])
-                    march_begin(m[j], E::div(vz0, ddf[j]), E::div(vz1, ddf[j]));
-                else {
-                    m[j].phase = 0;
-                    m[j].evals = 0;
-                    m[j].hit = false;
-                }
-            }
-            // lockstep march: one field evaluation per active ray per step
-            for (;;) {
-                const bool a0 = m[0].phase != 0, a1 = m[1].phase != 0;
-                const uint32_t both = __ballot_sync(kFull, a0 && a1);
-                const uint32_t anyA = __ballot_sync(kFull, a0 || a1);
-                if (anyA == 0u) break;
-                if (both != 0u) {
-                    F3 pts[2] = {ray_point<O>(cam.pos, dir[0], m[0].evalT),
-                                 ray_point<O>(cam.pos, dir[1], m[1].evalT)};
-                    float v[2];
-                    eval_view<O, 2>(s, t.words, pts, v);
-                    if (a0) march_consume(m[0], v[0], tp);
-                    if (a1) march_consume(m[1], v[1], tp);
-                } else {
-                    const int j = a0 ? 0 : 1;
-                    F3 pts[1] = {ray_point<O>(cam.pos, j == 0 ? dir[0] : dir[1],
-                                              j == 0 ? m[0].evalT : m[1].evalT)};
-                    float v[1];
-                    eval_view<O, 1>(s, t.words, pts, v);
-                    if (a0)
-                        march_consume(m[0], v[0], tp);
-                    else if (a1)
-                        march_consume(m[1], v[0], tp);
+            // Two ray slots per lane, served one after the other: `cur` is the
+            // slot being marched, `oth` the other one.  Each step evaluates the
+            // field once per lane (one instantiation of the evaluator keeps the
+            // hot loop inside the instruction cache).
+            RayLane cur, oth;
+            cur.slot = 0;
+            oth.slot = 1;
+            cur.dir = dir[0];
+            oth.dir = dir[1];
+            if (!found[0]) march_begin(cur.m, E::div(vz0, ddf[0]), E::div(vz1, ddf[0]));
+            else march_idle(cur.m);
+            if (!found[1]) march_begin(oth.m, E::div(vz0, ddf[1]), E::div(vz1, ddf[1]));
+            else march_idle(oth.m);
+            if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
+            while (__any_sync(kFull, cur.m.phase != 0)) {
+                const F3 p = ray_point<O>(cam.pos, cur.dir, cur.m.evalT);
+                const float v = eval_view<O>(s, t.words, p);
+                if (cur.m.phase != 0) {
+                    march_consume(cur.m, v, tp);
+                    if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
                 }
             }
             const uint32_t nView = s.nView, nPrim = s.nPrim, fl = s.flops;
+            const March& m0 = cur.slot == 0 ? cur.m : oth.m;
+            const March& m1 = cur.slot == 0 ? oth.m : cur.m;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
+                const March& mj = j == 0 ? m0 : m1;
                 if (found[j]) continue;
-                const uint32_t e = m[j].evals;
+                const uint32_t e = mj.evals;
                 evals[j] += e;
                 stFE += e;
                 stRNV += (uint64_t)e * nView;
                 stPE += (uint64_t)e * nPrim;
                 stFL += (uint64_t)e * fl;
-                if (m[j].hit) {
+                if (mj.hit) {
                     found[j] = true;
                     hitf[j] = true;
-                    depth[j] = m[j].hitT;
+                    depth[j] = mj.hitT;
                 }
             }
             __syncwarp();
@@ -286,28 +287,68 @@ __global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* cou
     }
 }
 
-// gradient_normal (tracer.cpp:285-294): lanes 0..5 evaluate the full tree at
-// p +- h e_axis, h = max(1e-3, 1e-4 t).
+// gradient_normal (tracer.cpp:285-294) with eval_full (traversal.cpp:126-141)
+// at p +- h e_axis, h = max(1e-3, 1e-4 t), for every queued pixel; one warp
+// per pixel.  Phase 1: the 32 lanes evaluate all primitives at the 6 taps
+// (independent work) into the warp's scratch.  Phase 2: lanes 0..5 run the
+// post-order operator program over those values (the same op order as the
+// reference walk, so exact mode stays bit-identical).
 template <class O>
 __global__ void __launch_bounds__(128) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
-                                                  const uint32_t* counters, uint64_t* stats) {
+                                                  const uint32_t* counters, uint64_t* stats, float* scratch,
+                                                  uint32_t scratchWarps) {
     const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = min((gridDim.x * blockDim.x) >> 5, scratchWarps);
     const uint32_t n = counters[kCntFallback];
-    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
+    if (warp >= nwarps) return;
+    float* sv = scratch + (size_t)warp * t.nprims * 6;
+    for (uint32_t i = warp; i < n; i += nwarps) {
         const uint32_t p = g.fallback[i];
         const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
         const F3 pc = position_at(cam, fb, g, x, y);
-        const float depth = g.depth[p];
-        const float h = smax(1e-3f, E::mul(1e-4f, depth));
+        const float h = smax(1e-3f, E::mul(1e-4f, g.depth[p]));
+        const F3 taps[6] = {{E::add(pc.x, h), pc.y, pc.z}, {E::sub(pc.x, h), pc.y, pc.z},
+                            {pc.x, E::add(pc.y, h), pc.z}, {pc.x, E::sub(pc.y, h), pc.z},
+                            {pc.x, pc.y, E::add(pc.z, h)}, {pc.x, pc.y, E::sub(pc.z, h)}};
+        for (uint32_t k = lane; k < t.nprims * 6u; k += 32) {
+            const uint32_t prim = k / 6u, tap = k - prim * 6u;
+            const uint32_t w = __ldg(&t.primWords[prim]);
+            float P[20];
+            load_params<5>(P, t.words + w + 1);
+            F3 q = taps[0];
+#pragma unroll
+            for (int j = 1; j < 6; ++j)
+                if (tap == (uint32_t)j) q = taps[j];
+            sv[k] = eval_primitive<O>(blob_op(tree_blob(t.words, w)), P, q);
+        }
+        __syncwarp();
         float v = 0.0f;
         if (lane < 6) {
-            F3 q = pc;
-            const int axis = lane >> 1;
-            if (axis == 0) q.x = (lane & 1) ? E::sub(pc.x, h) : E::add(pc.x, h);
-            if (axis == 1) q.y = (lane & 1) ? E::sub(pc.y, h) : E::add(pc.y, h);
-            if (axis == 2) q.z = (lane & 1) ? E::sub(pc.z, h) : E::add(pc.z, h);
-            v = eval_full<O>(t, q);
+            float stk[kFullStackCap];
+            int sp = 0;
+            uint32_t prim = 0;
+            for (uint32_t j = 0; j < t.nnodes; ++j) {
+                const uint32_t e = __ldg(&t.fullProgram[j]);
+                if (e >> 31) {
+                    stk[sp++] = sv[prim * 6u + lane];
+                    ++prim;
+                } else {
+                    const uint32_t code = (e >> 26) & 0x1Fu;
+                    float kd[2] = {0.f, 0.f};
+                    if (code >= 6u) {
+                        const float4 q = __ldg(t.words + (e & kSentinel) + 1);
+                        kd[0] = q.x;
+                        kd[1] = q.y;
+                    }
+                    const float right = stk[sp - 1], left = stk[sp - 2];
+                    stk[sp - 2] = eval_operator<O>(code, kd, left, right);
+                    --sp;
+                }
+            }
+            v = stk[0];
         }
         float f[6];
 #pragma unroll
@@ -319,9 +360,8 @@ __global__ void __launch_bounds__(128) k_gradient(DevTree t, Cam cam, FrameBufs 
             g.normal[3 * p + 1] = nn.y;
             g.normal[3 * p + 2] = nn.z;
         }
+        __syncwarp();
     }
-    if (threadIdx.x == 0 && blockIdx.x == 0)
-        atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
 }
 
 // oracle_render: one thread per pixel over [near, far], full tree.
@@ -381,14 +421,15 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
 
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
-                    uint64_t* stats, int smCount) {
+                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps) {
     cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
     dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
     k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
+    const uint32_t blocks = (scratchWarps + 3) / 4;
     if (exact)
-        k_gradient<ExactOps><<<smCount * 4, 128, 0, st>>>(t, cam, fb, g, counters, stats);
+        k_gradient<ExactOps><<<blocks, 128, 0, st>>>(t, cam, fb, g, counters, stats, scratch, scratchWarps);
     else
-        k_gradient<FastOps><<<smCount * 4, 128, 0, st>>>(t, cam, fb, g, counters, stats);
+        k_gradient<FastOps><<<blocks, 128, 0, st>>>(t, cam, fb, g, counters, stats, scratch, scratchWarps);
 }
 
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,

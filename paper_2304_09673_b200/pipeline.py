@@ -278,9 +278,10 @@ class Renderer:
         check(self.lib.bt_oracle_render(self.ctx, C.byref(cam), C.byref(c), int(exact)), "bt_oracle_render")
 
     def render_frame(self, cam: bt_camera, cfg: RenderConfig, exact: bool = False, graph: bool = True,
-                     tile0: int = 0, tile1: int = 0) -> None:
+                     tile0: int = 0, tile1: int = 0, normals: bool = True) -> None:
         c = cfg.to_c()
-        check(self.lib.bt_render_frame(self.ctx, C.byref(cam), C.byref(c), tile0, tile1, int(exact), int(graph)),
+        flags = (1 if graph else 0) | (0 if normals else 2)
+        check(self.lib.bt_render_frame(self.ctx, C.byref(cam), C.byref(c), tile0, tile1, int(exact), flags),
               "bt_render_frame")
 
     def download_gbuffer(self, out: GBuffer | None = None) -> GBuffer:

@@ -137,8 +137,9 @@ class RefScene:
         st = np.zeros(6, np.uint64)
         ms = np.zeros(2, np.float64)
         c = cfg.to_c()
-        _check(ref_lib().ref_render_tiles(self.h, C.byref(c), threads, ptr(np.ascontiguousarray(offsets, np.uint32)),
-                                          ptr(np.ascontiguousarray(frags, FRAG_DTYPE)), int(normals), ptr(g.hit),
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        frags = np.ascontiguousarray(frags, FRAG_DTYPE)
+        _check(ref_lib().ref_render_tiles(self.h, C.byref(c), threads, ptr(offsets), ptr(frags), int(normals), ptr(g.hit),
                                           ptr(g.depth), ptr(g.normal), ptr(g.evalCount), ptr(g.tileMaxOverlap),
                                           ptr(g.tileCacheBytes), ptr(g.tileError), ptr(st), ptr(ms)))
         return g, RefStats(*[int(v) for v in st]), ms
@@ -184,3 +185,109 @@ def compare_gbuffers(a: GBuffer, b: GBuffer, tol: float) -> dict:
                           ptr(out))
     return {"hitAgreement": out[0], "depthRms": out[1], "depthMax": out[2], "depthOutliers": int(out[3]),
             "hitMismatches": int(out[4])}
+
+
+# ---------------------------------------------------------------------------
+# C restatement (oracle/port/bt_port.c)
+
+_port = None
+
+
+class port_tree(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("nwords", C.c_uint32), ("nodes", C.c_void_p), ("nnodes", C.c_uint32),
+                ("prims", C.c_void_p), ("nprims", C.c_uint32)]
+
+
+def port_available() -> bool:
+    return os.path.exists(PORT_LIB)
+
+
+def port_lib() -> C.CDLL:
+    global _port
+    if _port is None:
+        lib = C.CDLL(PORT_LIB)
+        vp = C.c_void_p
+        T = C.POINTER(port_tree)
+        lib.port_roi.argtypes = [T, vp]
+        lib.port_vois.argtypes = [T, vp, C.c_float, vp]
+        lib.port_rasterize.argtypes = [vp, C.c_uint32, vp, vp, vp, C.c_uint64, vp]
+        lib.port_render_tiles.argtypes = [T, vp, vp, vp, vp, C.c_int] + [vp] * 7
+        lib.port_normals.argtypes = [T, vp, C.c_int, vp, vp, vp]
+        lib.port_oracle.argtypes = [T, vp, vp, C.c_int, vp, vp, vp, vp]
+        lib.port_eval_primitive.argtypes = [C.c_uint32, vp, C.c_float, C.c_float, C.c_float]
+        lib.port_eval_primitive.restype = C.c_float
+        lib.port_eval_operator.argtypes = [C.c_uint32, vp, C.c_float, C.c_float]
+        lib.port_eval_operator.restype = C.c_float
+        lib.port_eval_full.argtypes = [T, C.c_float, C.c_float, C.c_float]
+        lib.port_eval_full.restype = C.c_float
+        _port = lib
+    return _port
+
+
+class Port:
+    """The C restatement driven with a scene's compiled arrays."""
+
+    def __init__(self, data: np.ndarray, nodes: np.ndarray, prims: np.ndarray, device_camera, width: int,
+                 height: int):
+        self.data, self.nodes, self.prims = data, nodes, prims  # keep alive
+        self.t = port_tree(data.ctypes.data, len(data) // 4, nodes.ctypes.data, len(nodes), prims.ctypes.data,
+                           len(prims))
+        self.cam = device_camera
+        self.width, self.height = width, height
+
+    @classmethod
+    def from_scene(cls, scene) -> "Port":
+        return cls(scene.data.copy(), scene.nodes.copy(), scene.prims.copy(), scene.device_camera, scene.width,
+                   scene.height)
+
+    def roi(self) -> np.ndarray:
+        out = np.zeros(len(self.nodes), np.float32)
+        port_lib().port_roi(C.byref(self.t), ptr(out))
+        return out
+
+    def vois(self, margin: float) -> np.ndarray:
+        out = np.zeros(len(self.prims), VOI_DTYPE)
+        roi = self.roi()
+        port_lib().port_vois(C.byref(self.t), ptr(roi), C.c_float(margin), ptr(out))
+        return out
+
+    def rasterize(self, vois: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        vois = np.ascontiguousarray(vois, VOI_DTYPE)
+        tx, ty = (self.width + 7) // 8, (self.height + 7) // 8
+        offsets = np.zeros(tx * ty + 1, np.uint32)
+        total = C.c_uint64()
+        port_lib().port_rasterize(ptr(vois), len(vois), C.byref(self.cam), ptr(offsets), None, 0, C.byref(total))
+        frags = np.zeros(total.value, FRAG_DTYPE)
+        port_lib().port_rasterize(ptr(vois), len(vois), C.byref(self.cam), ptr(offsets), ptr(frags), total.value,
+                                  C.byref(total))
+        return offsets, frags
+
+    def render_tiles(self, cfg: RenderConfig, offsets, frags, threads: int = 1) -> tuple[GBuffer, np.ndarray]:
+        g = GBuffer.empty(self.width, self.height)
+        st = np.zeros(6, np.uint64)
+        c = cfg.to_c()
+        offsets = np.ascontiguousarray(offsets, np.uint32)
+        frags = np.ascontiguousarray(frags, FRAG_DTYPE)
+        port_lib().port_render_tiles(C.byref(self.t), C.byref(self.cam), C.byref(c), ptr(offsets), ptr(frags),
+                                     threads, ptr(g.hit), ptr(g.depth),
+                                     ptr(g.evalCount), ptr(g.tileMaxOverlap), ptr(g.tileCacheBytes),
+                                     ptr(g.tileError), ptr(st))
+        return g, st
+
+    def normals(self, g: GBuffer, mode: int = 0) -> None:
+        port_lib().port_normals(C.byref(self.t), C.byref(self.cam), mode, ptr(g.hit), ptr(g.depth), ptr(g.normal))
+
+    def frame(self, cfg: RenderConfig, threads: int = 1) -> tuple[GBuffer, np.ndarray, np.ndarray, np.ndarray]:
+        v = self.vois(cfg.hitEpsilon)
+        off, fr = self.rasterize(v)
+        g, st = self.render_tiles(cfg, off, fr, threads)
+        self.normals(g, cfg.normalsMode)
+        return g, st, off, fr
+
+    def oracle(self, cfg: RenderConfig, threads: int = 1) -> tuple[GBuffer, np.ndarray]:
+        g = GBuffer.empty(self.width, self.height)
+        st = np.zeros(6, np.uint64)
+        c = cfg.to_c()
+        port_lib().port_oracle(C.byref(self.t), C.byref(self.cam), C.byref(c), threads, ptr(g.hit), ptr(g.depth),
+                               ptr(g.evalCount), ptr(st))
+        return g, st

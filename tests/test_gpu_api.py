@@ -1,0 +1,193 @@
+"""GPU behaviour of the boundary (run with -m gpu): the reference's own unit
+tests against this library, graph replay, tile-range sharding, per-frame
+parameter updates, the brute-force oracle, tile errors and determinism."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle_bridge import Port, RefScene, compare_gbuffers, ref_available
+from paper_2304_09673_b200.pipeline import RenderConfig, Renderer, Scene
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def rd():
+    r = Renderer(0)
+    yield r
+    r.close()
+
+
+def test_reference_unit_tests_pass_against_b200_library():
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_unit_tests_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", p.stdout)
+    assert m and m.group(1) == "72" and m.group(2) == "72", p.stdout + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_graph_replay_equals_eager(rd, exact):
+    cfg = RenderConfig()
+    s = Scene.build("C3")
+    rd.upload(s)
+    rd.render_frame(s.device_camera, cfg, exact=exact, graph=False)
+    a = rd.download_gbuffer()
+    for _ in range(3):
+        rd.render_frame(s.device_camera, cfg, exact=exact, graph=True)
+    b = rd.download_gbuffer()
+    for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert getattr(a, plane).tobytes() == getattr(b, plane).tobytes(), plane
+
+
+@pytest.mark.parametrize("name,parts", [("C3", 3), ("C4", 4)])
+def test_tile_range_sharding_equals_full_frame(rd, name, parts):
+    """Multi-GPU partition, on one device: tracing tile-row ranges separately
+    reproduces the full frame (tiles never interact)."""
+    cfg = RenderConfig()
+    s = Scene.build(name)
+    rd.upload(s)
+    cam = s.device_camera
+    rd.render_frame(cam, cfg, exact=False, graph=False)
+    full = rd.download_gbuffer()
+    tx, ty = s.tiles
+    rows = np.linspace(0, ty, parts + 1).round().astype(int)
+    rd.build_volumes_of_interest(cfg.hitEpsilon)
+    for r in range(parts):
+        t0, t1 = int(rows[r] * tx), int(rows[r + 1] * tx)
+        rd.rasterize_volumes(cam, t0, t1)  # A-buffer of this shard only
+        rd.render_tiles(cam, cfg, exact=False, tile0=t0, tile1=t1)
+        part = rd.download_gbuffer()
+        lo, hi = rows[r] * 8 * s.width, min(rows[r + 1] * 8, s.height) * s.width
+        assert part.hit[lo:hi].tobytes() == full.hit[lo:hi].tobytes()
+        assert part.depth[lo:hi].tobytes() == full.depth[lo:hi].tobytes()
+        assert part.evalCount[lo:hi].tobytes() == full.evalCount[lo:hi].tobytes()
+
+
+def test_per_frame_parameter_updates_match_reference(rd):
+    cfg = RenderConfig()
+    s = Scene.build("C3")
+    rd.upload(s)
+    cam = s.device_camera
+    ref = RefScene("C3") if ref_available() else None
+    for f in (1, 2):
+        words, params, counts = s.perturb(f)
+        rd.update_params(words, params, counts)
+        assert rd.tree_words().tobytes() == s.data.tobytes()  # device words == host update_primitive_params
+        rd.render_frame(cam, cfg, exact=True, graph=True)
+        g = rd.download_gbuffer()
+        if ref is not None:
+            ref.perturb(f)
+            gr, _, _, _ = ref.frame(cfg)
+        else:
+            gr, _, _, _ = Port.from_scene(s).frame(cfg, threads=os.cpu_count() or 4)
+        assert g.hit.tobytes() == gr.hit.tobytes()
+        assert g.depth.tobytes() == gr.depth.tobytes()
+        assert g.normal.tobytes() == gr.normal.tobytes()
+
+
+def test_oracle_render_and_pipeline_agree(rd):
+    """test_tracer.cpp:226-247: pipeline vs brute-force oracle on a CSG scene."""
+    cfg = RenderConfig()
+    s = Scene.build("csg")
+    rd.upload(s)
+    cam = s.device_camera
+    rd.oracle_render(cam, cfg, exact=True)
+    go = rd.download_gbuffer()
+    rd.render_frame(cam, cfg, exact=False, graph=False)
+    gp = rd.download_gbuffer()
+    if ref_available():
+        rep = compare_gbuffers(gp, go, 2 * cfg.minStep)
+        assert rep["hitAgreement"] >= 0.995 and rep["depthRms"] <= 2 * cfg.minStep
+    m = (go.hit == 1) & (gp.hit == 1)
+    assert (go.hit == gp.hit).mean() >= 0.995
+    assert np.sqrt(np.mean((go.depth[m].astype(np.float64) - gp.depth[m]) ** 2)) <= 2 * cfg.minStep
+
+
+def test_oracle_render_c1_matches_reference(rd):
+    cfg = RenderConfig()
+    s = Scene.build("C1", 0, 128, 128)
+    rd.upload(s)
+    rd.reset_stats()
+    rd.oracle_render(s.device_camera, cfg, exact=True)
+    g = rd.download_gbuffer()
+    st = rd.stats()
+    go, so = (RefScene("C1", 0, 128, 128).oracle(cfg) if ref_available()
+              else Port.from_scene(s).oracle(cfg, threads=os.cpu_count() or 4))
+    assert g.hit.tobytes() == go.hit.tobytes() and g.depth.tobytes() == go.depth.tobytes()
+    assert g.evalCount.tobytes() == go.evalCount.tobytes()
+
+
+def test_tile_errors_mark_tiles_and_render_continues(rd):
+    """test_tracer.cpp:249-266: a 25-deep right comb overflows the stack."""
+    cfg = RenderConfig()
+    s = Scene.build("comb_error")
+    rd.upload(s)
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    g = rd.download_gbuffer()
+    assert g.tileError.any() and not g.tileError.all()
+    assert rd.stats().tileErrors == int(g.tileError.sum())
+
+
+def test_render_is_deterministic(rd):
+    cfg = RenderConfig()
+    s = Scene.build("C5")
+    rd.upload(s)
+    outs = []
+    for _ in range(2):
+        rd.render_frame(s.device_camera, cfg, exact=False, graph=False)
+        g = rd.download_gbuffer()
+        off, frags = rd.download_abuffer()
+        outs.append((g.hit.tobytes(), g.depth.tobytes(), g.evalCount.tobytes(), off.tobytes(), frags.tobytes()))
+    assert outs[0] == outs[1]
+
+
+def test_c4_exact_vs_fast_agreement(rd):
+    cfg = RenderConfig()
+    s = Scene.build("C4")
+    rd.upload(s)
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    ge = rd.download_gbuffer()
+    rd.render_frame(s.device_camera, cfg, exact=False, graph=True)
+    gf = rd.download_gbuffer()
+    assert (ge.hit == gf.hit).mean() >= 0.999
+    assert ge.hit.sum() > 0.2 * len(ge.hit)
+
+
+def test_central_difference_normals_exact(rd):
+    cfg = RenderConfig(normalsMode=1)
+    s = Scene.build("csg", 0, 64, 64)
+    rd.upload(s)
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    g = rd.download_gbuffer()
+    gr, _, _, _ = (RefScene("csg", 0, 64, 64).frame(cfg) if ref_available()
+                   else Port.from_scene(s).frame(cfg, threads=4))
+    assert g.normal.tobytes() == gr.normal.tobytes()
+
+
+def test_invalid_config_raises_before_device(rd):
+    s = Scene.build("sphere")
+    rd.upload(s)
+    with pytest.raises(ValueError, match="relaxation"):
+        rd.render_frame(s.device_camera, RenderConfig(relax=2.5))
+
+
+def test_external_torch_stream(rd):
+    import torch
+    cfg = RenderConfig()
+    s = Scene.build("C1")
+    rd.upload(s)
+    st = torch.cuda.Stream()
+    rd.set_stream(st.cuda_stream)
+    with torch.cuda.stream(st):
+        rd.render_frame(s.device_camera, cfg, exact=True, graph=True)
+    st.synchronize()
+    g = rd.download_gbuffer()
+    rd.set_stream(0)
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    assert rd.download_gbuffer().hit.tobytes() == g.hit.tobytes()

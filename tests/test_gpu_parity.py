@@ -1,0 +1,169 @@
+"""GPU parity (run on a B200 with -m gpu): every stage of the CUDA path
+against the CPU oracle on identical scenes, through the C-ABI.
+
+Contract:
+  * exact mode (IEEE op-by-op kernels): ROI, VOIs, A-buffer CSR (membership,
+    order, zEntry/zExit bits), G-buffer (hit, depth, evalCount, normals,
+    tile planes) and RenderStats are BIT-IDENTICAL to the reference;
+  * fast mode (FMA-contracted field evaluation): hit mask >= 99.9 %, matched
+    depth |dt| <= 2*minStep everywhere and <= 1e-4*t on >= 99.9 %, normal
+    dot >= 0.999 on >= 99.5 % of matched hits.
+The checker is the unmodified reference (oracle/_ref) when it was built,
+else the C restatement (oracle/_port), which tests/test_oracle_port.py pins
+to the reference bit for bit.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bridge import Port, RefScene, ref_available
+from paper_2304_09673_b200.pipeline import FRAG_DTYPE, VOI_DTYPE, RenderConfig, Renderer, Scene
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SCENES = [("sphere", 0, 0), ("csg", 0, 0), ("slab", 0, 0), ("comb_error", 0, 0), ("random:24", 0, 0),
+          ("C1", 0, 0), ("C2", 0, 0), ("C3", 0, 0), ("C5", 0, 0), ("gen:cells:167:hex:smooth", 0, 0),
+          ("gen:cells:334:tri:sharp", 0, 0), ("gen:grid:2:mixed:smooth", 0, 0)]
+
+
+def same(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    return a.nbytes == b.nbytes and a.view(np.uint8).tobytes() == b.view(np.uint8).tobytes()
+
+
+class Checker:
+    """Reference (preferred) or C restatement on the same scene."""
+
+    def __init__(self, scene: Scene, name, seed, w, h):
+        self.ref = RefScene(name, seed, w, h) if ref_available() else None
+        self.port = Port.from_scene(scene)
+
+    def roi(self):
+        return self.ref.roi() if self.ref else self.port.roi()
+
+    def vois(self, margin):
+        return self.ref.vois(margin) if self.ref else self.port.vois(margin)
+
+    def rasterize(self, vois):
+        return self.ref.rasterize(vois)[:2] if self.ref else self.port.rasterize(vois)
+
+    def render(self, cfg, off, frags):
+        if self.ref:
+            g, st, _ = self.ref.render_tiles(cfg, off, frags, threads=0, normals=True)
+            return g, [st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals, st.treeNodeCount, st.maxOverlap,
+                       st.maxCacheBytes]
+        g, st = self.port.render_tiles(cfg, off, frags, threads=os.cpu_count() or 4)
+        self.port.normals(g, cfg.normalsMode)
+        return g, list(st)
+
+
+@pytest.fixture(scope="module")
+def rd():
+    r = Renderer(0)
+    yield r
+    r.close()
+
+
+@pytest.mark.parametrize("name,w,h", SCENES, ids=[s[0] for s in SCENES])
+def test_exact_pipeline_is_bit_identical(rd, name, w, h):
+    seed = 7 if name.startswith("gen") else 0
+    cfg = RenderConfig()
+    s = Scene.build(name, seed, w, h)
+    chk = Checker(s, name, seed, w, h)
+    rd.upload(s)
+    cam = s.device_camera
+    # (a)
+    assert same(rd.propagate_roi(), chk.roi())
+    vois = rd.build_volumes_of_interest(cfg.hitEpsilon)
+    vois_ref = chk.vois(cfg.hitEpsilon)
+    assert same(vois, vois_ref)
+    # (b)
+    off, frags = rd.rasterize_volumes(cam)
+    off_ref, frags_ref = chk.rasterize(vois_ref)
+    assert same(off, off_ref), "per-tile fragment counts differ"
+    assert same(frags, frags_ref), "fragment lists differ"
+    # (c) + normals
+    rd.reset_stats()
+    rd.render_tiles(cam, cfg, exact=True)
+    rd.compute_normals(cam, 0, exact=True)
+    g = rd.download_gbuffer()
+    st = rd.stats()
+    gr, st_ref = chk.render(cfg, off_ref, frags_ref)
+    for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert same(getattr(g, plane), getattr(gr, plane)), plane
+    assert [st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals, st.treeNodeCount, st.maxOverlap,
+            st.maxCacheBytes] == st_ref
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5", "gen:cells:167:hex:smooth"])
+def test_fast_mode_within_tolerance(rd, name):
+    seed = 7 if name.startswith("gen") else 0
+    cfg = RenderConfig()
+    s = Scene.build(name, seed)
+    rd.upload(s)
+    cam = s.device_camera
+    rd.render_frame(cam, cfg, exact=True, graph=False)
+    ge = rd.download_gbuffer()  # == reference (previous test)
+    rd.render_frame(cam, cfg, exact=False, graph=True)
+    gf = rd.download_gbuffer()
+    assert (ge.hit == gf.hit).mean() >= 0.999
+    m = (ge.hit == 1) & (gf.hit == 1)
+    dt = np.abs(ge.depth[m].astype(np.float64) - gf.depth[m])
+    assert dt.max() <= 2 * cfg.minStep + 1e-6
+    assert (dt <= 1e-4 * ge.depth[m]).mean() >= 0.999
+    dots = (ge.normal[m] * gf.normal[m]).sum(1)
+    assert (dots >= 0.999).mean() >= 0.995
+    assert (ge.tileError == gf.tileError).all()
+
+
+GOLDEN_FILES = sorted(glob.glob(os.path.join(GOLDEN, "scene_*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN_FILES, ids=[os.path.basename(p) for p in GOLDEN_FILES])
+def test_gpu_reproduces_golden_fixture(rd, path):
+    z = np.load(path)
+    name, w, h = str(z["name"]), int(z["width"]), int(z["height"])
+    cfg = RenderConfig()
+    s = Scene.build(name, 0, w, h)
+    rd.upload(s)
+    cam = s.device_camera
+    assert rd.propagate_roi().tobytes() == z["roi"].tobytes()
+    assert rd.build_volumes_of_interest(cfg.hitEpsilon).view(np.uint8).tobytes() == z["vois"].tobytes()
+    off, frags = rd.rasterize_volumes(cam)
+    assert off.tobytes() == z["offsets"].tobytes() and frags.view(np.uint8).tobytes() == z["frags"].tobytes()
+    rd.reset_stats()
+    rd.render_tiles(cam, cfg, exact=True)
+    rd.compute_normals(cam, 0, exact=True)
+    g = rd.download_gbuffer()
+    for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert getattr(g, plane).tobytes() == z[plane].tobytes(), plane
+    st = rd.stats()
+    assert [st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals, st.treeNodeCount, st.maxOverlap,
+            st.maxCacheBytes] == list(z["stats"])
+    if "oracle_hit" in z:
+        rd.reset_stats()
+        rd.oracle_render(cam, cfg, exact=True)
+        go = rd.download_gbuffer()
+        assert go.hit.tobytes() == z["oracle_hit"].tobytes()
+        assert go.depth.tobytes() == z["oracle_depth"].tobytes()
+        assert go.evalCount.tobytes() == z["oracle_evalCount"].tobytes()
+        so = rd.stats()
+        assert [so.fieldEvals, so.retainedNodeVisits, so.primitiveEvals] == list(z["oracle_stats"])
+
+
+def test_abuffer_from_uploaded_reference_volumes(rd):
+    """rasterize_volumes on caller volumes (the compat entry point): arbitrary
+    volume order and duplicate words keep the reference's stable order."""
+    cfg = RenderConfig()
+    s = Scene.build("random:24")
+    chk = Checker(s, "random:24", 0, 0, 0)
+    rd.upload(s)
+    v = chk.vois(cfg.hitEpsilon)
+    v = np.concatenate([v[::-1], v[:5]])  # reversed + duplicates
+    rd.upload_volumes(v)
+    off, frags = rd.rasterize_volumes(s.device_camera)
+    off_ref, frags_ref = chk.rasterize(v)
+    assert same(off, off_ref) and same(frags, frags_ref)
