@@ -21,7 +21,15 @@ struct DevTree {
     const uint32_t* fullProgram = nullptr; // post-order (isPrim<<31 | op<<26 | word)
     uint32_t nwords = 0, nnodes = 0, nprims = 0;
     uint32_t fullDepth = 0;                // max stack depth of a full post-order walk
+    // frontier decomposition of the full tree (gradient-normal fallback):
+    // subtrees of <= kFrontierMax nodes, evaluated in parallel, then the
+    // remaining upper operators in post-order over their values
+    const uint2* frontier = nullptr;       // ordinal range [lo, hi] per subtree
+    const uint32_t* upperProgram = nullptr;// bit31 ? load frontier value : (op<<26 | word)
+    uint32_t nFrontier = 0, nUpper = 0;
 };
+constexpr uint32_t kFrontierMax = 32;
+constexpr size_t kGradSmemBytes = 160 * 1024;  // frontier values kept in shared memory up to this size
 
 struct FrameBufs {
     // camera products
@@ -29,6 +37,8 @@ struct FrameBufs {
     float4* cones = nullptr;     // [tiles] axis.xyz, cos
     float* coneSin = nullptr;    // [tiles]
     float4* sbCones = nullptr;   // [superblocks] axis.xyz, half-angle (rad, conservative)
+    float4* tileFrustum = nullptr; // [tiles*4] inward unit normals of the pixel-centre pyramid
+    float4* sbFrustum = nullptr;   // [superblocks*4] same for the superblock
     // A-buffer
     uint2* pairs = nullptr;      // (voi, superblock)
     uint4* pool = nullptr;       // (tile, voi, entry bits, exit bits), unsorted
@@ -114,7 +124,8 @@ void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t t
 // ---- launchers (k_trace.cu) -------------------------------------------
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                   const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
-                  uint32_t tile0, uint32_t tile1);
+                  uint32_t tile0, uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue);
+size_t trace_scratch_float4s(int smCount);
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps);

@@ -24,6 +24,18 @@
 
 namespace btk {
 
+// float4 units of a view node's precomputed parameter block (tolerance
+// path, see bt_fast.cuh): affine rows for rotated primitives, reciprocals,
+// operator constants.
+BT_HD uint32_t fast_block_size(uint32_t blob) {
+    if (blob_is_prim(blob)) {
+        const uint32_t k = blob_op(blob);
+        return k == 0u ? 1u : k == 1u ? 5u : k == 2u ? 4u : k == 3u ? 4u : k == 4u ? 5u : 6u;
+    }
+    const uint32_t c = blob_op(blob);
+    return (c >= 6u && c <= 8u) ? 1u : (c >= 9u && c <= 11u) ? 2u : 0u;
+}
+
 // Tile error codes (tileError is 1 for either, like the reference's catch).
 constexpr uint32_t kErrStack = 1;
 constexpr uint32_t kErrView = 2;
@@ -31,6 +43,7 @@ constexpr uint32_t kErrLogic = 3;
 
 constexpr int kFragStage = 128;  // fragments of a tile list staged in shared memory
 constexpr int kViewCap = 2 * kMaxOverlap - 1;
+constexpr uint32_t kFastBlockCap = kViewCap * 6;  // float4s per warp
 
 struct TraceParams {
     float L, invL, relax, minStep, hitEps;
@@ -52,11 +65,12 @@ struct WarpSmem {
     // pruned view: blob (op possibly rewritten) and the source word of params
     uint32_t vBlob[kViewCap];
     uint32_t vWord[kViewCap];
+    uint16_t vOff[kViewCap];  // float4 offset of the node's fast parameter block
     // view-build traversal stack
     uint32_t sBlob[kStackCap];
     uint8_t sUse[kStackCap];
     // published scalars
-    uint32_t nAct, cursor, nView, nPrim, rootUsed, maxDepth, flops, cacheFloats, err, done;
+    uint32_t nAct, cursor, nView, nPrim, rootUsed, maxDepth, flops, cacheFloats, err, done, vEnd;
     float zBegin, zEnd;
 };
 
@@ -157,6 +171,8 @@ BT_DEV void view_append(WarpSmem& s, uint32_t blob, uint32_t word, bool copyPara
     if (floats > 0u && s.cacheFloats + floats <= kCacheFloats) s.cacheFloats += floats;
     s.vBlob[s.nView] = blob;
     s.vWord[s.nView] = word;
+    s.vOff[s.nView] = (uint16_t)s.vEnd;
+    s.vEnd += fast_block_size(blob);
     s.nView++;
 }
 
@@ -164,6 +180,7 @@ BT_DEV void build_view(WarpSmem& s, const float4* words) {
     const uint32_t n = s.nAct;
     s.nView = 0;
     s.nPrim = 0;
+    s.vEnd = 0;
     s.cacheFloats = 0;
     s.rootUsed = 0;
     s.maxDepth = 0;

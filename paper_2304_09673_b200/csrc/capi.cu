@@ -80,7 +80,9 @@ struct bt_ctx {
 
     // tree
     DevBuf<float4> words;
-    DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram;
+    DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram;
+    DevBuf<uint2> frontier;
+    uint32_t nFrontier = 0, nUpper = 0;
     DevBuf<int32_t> compactAnc;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
@@ -94,7 +96,7 @@ struct bt_ctx {
 
     // frame
     int width = 0, height = 0, tilesX = 0, tilesY = 0;
-    DevBuf<float4> rays, cones, sbCones;
+    DevBuf<float4> rays, cones, sbCones, tileFrustum, sbFrustum;
     DevBuf<float> coneSin;
     DevBuf<uint2> pairs;
     DevBuf<uint4> pool, unsorted;
@@ -111,6 +113,8 @@ struct bt_ctx {
     bool haveGbuffer = false;
 
     DevBuf<uint64_t> stats;
+    DevBuf<float4> traceScratch;  // per-warp fast parameter blocks of k_trace
+    DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
 
@@ -141,6 +145,10 @@ DevTree dev_tree(const bt_ctx* c) {
     t.nnodes = c->nnodes;
     t.nprims = c->nprims;
     t.fullDepth = c->fullDepth;
+    t.frontier = c->frontier.ptr;
+    t.upperProgram = c->upperProgram.ptr;
+    t.nFrontier = c->nFrontier;
+    t.nUpper = c->nUpper;
     return t;
 }
 
@@ -150,6 +158,8 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.cones = c->cones.ptr;
     f.coneSin = c->coneSin.ptr;
     f.sbCones = c->sbCones.ptr;
+    f.tileFrustum = c->tileFrustum.ptr;
+    f.sbFrustum = c->sbFrustum.ptr;
     f.pairs = c->pairs.ptr;
     f.pool = c->pool.ptr;
     f.unsorted = c->unsorted.ptr;
@@ -210,6 +220,8 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->cones.reserve(tiles));
     BT_CUDA(c->coneSin.reserve(tiles));
     BT_CUDA(c->sbCones.reserve(nsb));
+    BT_CUDA(c->tileFrustum.reserve(tiles * 4));
+    BT_CUDA(c->sbFrustum.reserve(nsb * 4));
     BT_CUDA(c->tileCount.reserve(tiles));
     BT_CUDA(c->tileCursor.reserve(tiles));
     BT_CUDA(c->tileLocal.reserve(tiles));
@@ -334,8 +346,13 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
 
 int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
              int exact) {
+    if (c->traceScratch.cap == 0) {
+        BT_CUDA(c->traceScratch.reserve(trace_scratch_float4s(c->smCount)));
+        BT_CUDA(c->tileQueue.reserve(1));
+        c->bufEpoch++;
+    }
     launch_trace(c->stream, exact != 0, dev_tree(c), to_cam(cam), trace_params(cfg, cam), frame_bufs(c), gbuf(c),
-                 c->stats.ptr, tile0, tile1);
+                 c->stats.ptr, tile0, tile1, c->smCount, c->traceScratch.ptr, c->tileQueue.ptr);
     c->haveGbuffer = true;
     return BT_OK;
 }
@@ -343,11 +360,17 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
 int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
     if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
     if (c->gradWarps == 0) {
-        // up to 4 warps per SM, at most ~256 MiB of scratch for huge trees
-        const size_t per = (size_t)c->nprims * 6;
-        size_t warps = std::min<size_t>((size_t)c->smCount * 4, std::max<size_t>(1, (256u << 20) / (per * 4)));
-        BT_CUDA(c->gradScratch.reserve(warps * per));
-        c->gradWarps = (uint32_t)warps;
+        // one CTA per queued pixel; frontier values live in shared memory,
+        // or (very large trees) in a per-CTA global scratch
+        const size_t per = (size_t)c->nFrontier * 6;
+        size_t ctas = (size_t)c->smCount * 2;
+        if (per * 4 + (size_t)c->nUpper * 4 > kGradSmemBytes) {
+            ctas = std::min<size_t>(ctas, std::max<size_t>(1, (256u << 20) / (per * 4)));
+            BT_CUDA(c->gradScratch.reserve(ctas * per));
+        } else {
+            BT_CUDA(c->gradScratch.reserve(1));
+        }
+        c->gradWarps = (uint32_t)ctas;
         c->bufEpoch++;
     }
     launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
@@ -399,7 +422,8 @@ int bt_ctx_destroy(bt_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->graph) cudaGraphExecDestroy(c->graph);
-    for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->pWords, &c->pCounts,
+    c->frontier.release();
+    for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->upperProgram, &c->pWords, &c->pCounts,
                     &c->tileCount, &c->tileCursor, &c->tileLocal, &c->blockSum, &c->blockPrefix, &c->offsets,
                     &c->counters, &c->evalCount, &c->tileMaxOverlap, &c->tileCacheBytes, &c->fallback})
         b->release();
@@ -411,6 +435,8 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->rays.release();
     c->cones.release();
     c->sbCones.release();
+    c->tileFrustum.release();
+    c->sbFrustum.release();
     c->coneSin.release();
     c->pairs.release();
     c->pool.release();
@@ -422,6 +448,8 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->normal.release();
     c->stats.release();
     c->gradScratch.release();
+    c->traceScratch.release();
+    c->tileQueue.release();
     cudaEventDestroy(c->ev[0]);
     cudaEventDestroy(c->ev[1]);
     cudaStreamDestroy(c->own);
@@ -487,6 +515,23 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
             if (nodes[i].isPrimitive && nodes[i].word == primitiveWords[k]) primOrd[k++] = i;
         if (k != nprims) return fail(BT_EINVAL, "primitiveWords do not match the node records");
     }
+    // frontier decomposition: subtree sizes in post-order, frontier roots are
+    // the maximal subtrees of <= kFrontierMax nodes
+    std::vector<uint32_t> size(nnodes, 1);
+    for (uint32_t i = 0; i < nnodes; ++i)
+        if (!nodes[i].isPrimitive) size[i] = 1 + size[nodes[i].leftChild] + size[nodes[i].rightChild];
+    std::vector<uint2> frontier;
+    std::vector<uint32_t> upper;
+    for (uint32_t i = 0; i < nnodes; ++i) {
+        const int32_t p = parentOrd[i];
+        const bool isRoot = size[i] <= kFrontierMax && (p < 0 || size[p] > kFrontierMax);
+        if (isRoot) {
+            upper.push_back(0x80000000u | (uint32_t)frontier.size());
+            frontier.push_back(make_uint2(i + 1 - size[i], i));
+        } else if (size[i] > kFrontierMax) {
+            upper.push_back(program[i]);  // operator (size > 1)
+        }
+    }
     // full post-order stack depth
     uint32_t depth = 0, maxd = 0;
     for (uint32_t i = 0; i < nnodes; ++i) {
@@ -506,6 +551,8 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(c->compactAnc.reserve(nnodes));
     BT_CUDA(c->fullProgram.reserve(nnodes));
     BT_CUDA(c->roi.reserve(nnodes));
+    BT_CUDA(c->frontier.reserve(frontier.size()));
+    BT_CUDA(c->upperProgram.reserve(upper.size()));
     BT_CUDA(c->vois.reserve(nprims));
     BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
     BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
@@ -514,6 +561,11 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->nodeWord.ptr, nodeWord.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->compactAnc.ptr, compactAnc.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->fullProgram.ptr, program.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->frontier.ptr, frontier.data(), frontier.size() * sizeof(uint2), cudaMemcpyHostToDevice,
+                            c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->upperProgram.ptr, upper.data(), upper.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    c->nFrontier = (uint32_t)frontier.size();
+    c->nUpper = (uint32_t)upper.size();
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->nwords = nwords;
     c->nnodes = nnodes;

@@ -72,6 +72,51 @@ __global__ void k_voi(DevTree t, const float* roi, float margin, Voi* vois) {
 
 // ---------------------------------------------------------------- camera
 
+// Pyramid spanned by the pixel-centre rays of a pixel rectangle
+// [x0, x1] x [y0, y1] (inclusive pixel indices).  Ray directions are affine
+// in the pixel coordinates before normalisation, so every pixel ray of the
+// rectangle lies inside the pyramid of its four corner rays: a volume that
+// misses the pyramid cannot be hit by any of them.  Writes 4 inward unit
+// plane normals (through the camera position).
+__device__ void pixel_pyramid(const Cam& c, int x0, int y0, int x1, int y1, float4* out) {
+    auto dir = [&](int px, int py) {
+        const float sx = ((2.0f * (px + 0.5f)) / c.width - 1.0f) * c.tanHalf * c.aspect;
+        const float sy = (1.0f - (2.0f * (py + 0.5f)) / c.height) * c.tanHalf;
+        return F3{c.fwd.x + c.right.x * sx + c.up.x * sy, c.fwd.y + c.right.y * sx + c.up.y * sy,
+                  c.fwd.z + c.right.z * sx + c.up.z * sy};
+    };
+    const F3 d[4] = {dir(x0, y0), dir(x1, y0), dir(x1, y1), dir(x0, y1)};
+    const F3 mid{0.25f * (d[0].x + d[1].x + d[2].x + d[3].x), 0.25f * (d[0].y + d[1].y + d[2].y + d[3].y),
+                 0.25f * (d[0].z + d[1].z + d[2].z + d[3].z)};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const F3 a = d[e], b = d[(e + 1) & 3];
+        F3 n{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+        float len = sqrtf(n.x * n.x + n.y * n.y + n.z * n.z);
+        if (len > 0.0f) {
+            n = F3{n.x / len, n.y / len, n.z / len};
+            if (n.x * mid.x + n.y * mid.y + n.z * mid.z < 0.0f) n = F3{-n.x, -n.y, -n.z};
+        } else {
+            n = F3{0.f, 0.f, 0.f};  // degenerate edge (1-pixel rectangle side): never rejects
+        }
+        out[e] = make_float4(n.x, n.y, n.z, 0.0f);
+    }
+}
+
+// Conservative sphere-vs-pyramid test with a relative + absolute pad that
+// dominates every FP32 rounding on both sides.
+__device__ __forceinline__ bool pyramid_may_touch(const float4* pl, F3 apex, const Sphere& s) {
+    const float vx = s.c.x - apex.x, vy = s.c.y - apex.y, vz = s.c.z - apex.z;
+    const float dist = sqrtf(vx * vx + vy * vy + vz * vz);
+    const float pad = 1e-4f * (dist + fabsf(s.r)) + 1e-5f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float4 n = pl[e];
+        if (n.x * vx + n.y * vy + n.z * vz < -(s.r + pad)) return false;
+    }
+    return true;
+}
+
 // One CTA per superblock: 4096 rays, 64 tile cones, 1 conservative
 // superblock cone containing all of its tile cones.
 __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY) {
@@ -95,6 +140,8 @@ __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tiles
         const bool valid = tx < tilesX && ty < tilesY;
         sValid[lt] = valid;
         if (valid) {
+            const int x1 = min(tx * kTile + kTile, cam.width) - 1, y1 = min(ty * kTile + kTile, cam.height) - 1;
+            pixel_pyramid(cam, tx * kTile, ty * kTile, x1, y1, fb.tileFrustum + (size_t)(ty * tilesX + tx) * 4);
             const Cone c = tile_cone(cam, tx, ty);
             const float4 v = make_float4(c.axis.x, c.axis.y, c.axis.z, c.cosH);
             fb.cones[ty * tilesX + tx] = v;
@@ -102,6 +149,11 @@ __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tiles
             sCone[lt] = v;
             sSin[lt] = c.sinH;
         }
+    }
+    if (threadIdx.x == 64) {
+        const int x0 = sx * kSB * kTile, y0 = sy * kSB * kTile;
+        const int x1 = min(x0 + kSB * kTile, cam.width) - 1, y1 = min(y0 + kSB * kTile, cam.height) - 1;
+        pixel_pyramid(cam, x0, y0, x1, y1, fb.sbFrustum + (size_t)blockIdx.x * 4);
     }
     __syncthreads();
     // superblock cone: axis = normalized sum of tile axes, half-angle =
@@ -184,7 +236,9 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
             const uint32_t first = (uint32_t)(sy * kSB * tilesX + sx * kSB);
             const int lastTy = min(sy * kSB + kSB, tilesY) - 1, lastTx = min(sx * kSB + kSB, tilesX) - 1;
             const uint32_t last = (uint32_t)(lastTy * tilesX + lastTx);
-            if (last >= tile0 && first < tile1) pass = sb_may_touch(fb.sbCones[sb], cam.pos, bs);
+            if (last >= tile0 && first < tile1)
+                pass = pyramid_may_touch(fb.sbFrustum + (size_t)sb * 4, cam.pos, bs) &&
+                       sb_may_touch(fb.sbCones[sb], cam.pos, bs);
         }
         const uint32_t m = __ballot_sync(kFull, pass);
         if (m == 0u) continue;
@@ -223,7 +277,10 @@ __global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameB
                 k.axis = F3{c.x, c.y, c.z};
                 k.cosH = c.w;
                 k.sinH = fb.coneSin[tiles[h]];
-                pass[h] = cone_may_touch(k, cam.pos, bs);
+                // exact reference cull (abuffer.cpp:193-196) and the pixel-centre
+                // pyramid (rays outside it cannot hit: skips empty ray sweeps)
+                pass[h] = cone_may_touch(k, cam.pos, bs) &&
+                          pyramid_may_touch(fb.tileFrustum + (size_t)tiles[h] * 4, cam.pos, bs);
             }
         }
         uint64_t mask = (uint64_t)__ballot_sync(kFull, pass[0]) | ((uint64_t)__ballot_sync(kFull, pass[1]) << 32);

@@ -15,7 +15,10 @@
 //
 // O = ExactOps gives bit-identical results to the CPU reference; O = FastOps
 // lets nvcc contract the field arithmetic into FFMA (tolerance path).
+#include <algorithm>
+
 #include "bt_device.h"
+#include "bt_fast.cuh"
 
 namespace btk {
 
@@ -47,16 +50,18 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     return v;
 }
 
+template <class O> struct IsFast {
+    static constexpr bool value = false;
+};
+template <> struct IsFast<FastOps> {
+    static constexpr bool value = true;
+};
+
+// One 8x8 tile, executed by one warp (see the file comment).
 template <class O>
-__global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam cam, TraceParams tp,
-                                                            FrameBufs fb, GBuf g, uint64_t* stats,
-                                                            uint32_t tile0, uint32_t tile1) {
-    extern __shared__ __align__(16) unsigned char smemRaw[];
-    WarpSmem* smem = reinterpret_cast<WarpSmem*>(smemRaw);
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& s = smem[wid];
-    const uint32_t tile = tile0 + blockIdx.x * kTraceWarps + wid;
-    if (tile >= tile1) return;
+__device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
+                                           const FrameBufs& fb, const GBuf& g, uint64_t* stats, WarpSmem& s,
+                                           float4* prm, int lane, uint32_t tile) {
     const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
 
     int px[2], py[2];
@@ -124,6 +129,11 @@ __global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam ca
                 tileErr = 1;
                 break;
             }
+            if (IsFast<O>::value) {  // lane-parallel parameter-block conversion
+                for (uint32_t i = lane; i < s.nView; i += 32)
+                    convert_node(s.vBlob[i], t.words + s.vWord[i] + 1, prm + s.vOff[i]);
+                __syncwarp();
+            }
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
             // Two ray slots per lane, served one after the other: `cur` is the
             // slot being marched, `oth` the other one.  Each step evaluates the
@@ -139,9 +149,13 @@ __global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam ca
             if (!found[1]) march_begin(oth.m, E::div(vz0, ddf[1]), E::div(vz1, ddf[1]));
             else march_idle(oth.m);
             if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
+            // (evaluating both slots in one pass was measured slower: as soon as
+            // one lane has two live rays the whole warp pays two evaluations)
             while (__any_sync(kFull, cur.m.phase != 0)) {
                 const F3 p = ray_point<O>(cam.pos, cur.dir, cur.m.evalT);
-                const float v = eval_view<O>(s, t.words, p);
+                float v;
+                if (IsFast<O>::value) eval_view_fast<1>(s, prm, &p, &v);
+                else v = eval_view<O>(s, t.words, p);
                 if (cur.m.phase != 0) {
                     march_consume(cur.m, v, tp);
                     if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
@@ -195,6 +209,28 @@ __global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam ca
         if (tileMaxOv) atomicMax((unsigned long long*)&stats[kStMaxOverlap], (unsigned long long)tileMaxOv);
         if (tileCache) atomicMax((unsigned long long*)&stats[kStMaxCache], (unsigned long long)tileCache);
         if (tileErr) atomicAdd((unsigned long long*)&stats[kStTileErrors], 1ull);
+    }
+}
+
+// Persistent kernel: each warp pulls tiles from a queue (tiles differ wildly
+// in cost -- empty tiles exit at once) and owns a fixed slot of the fast
+// parameter-block scratch.
+template <class O>
+__global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam cam, TraceParams tp, FrameBufs fb,
+                                                            GBuf g, uint64_t* stats, uint32_t tile0, uint32_t tile1,
+                                                            float4* fastScratch, uint32_t* tileQueue) {
+    extern __shared__ __align__(16) unsigned char smemRaw[];
+    WarpSmem* smem = reinterpret_cast<WarpSmem*>(smemRaw);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& s = smem[wid];
+    float4* prm = fastScratch + (size_t)(blockIdx.x * kTraceWarps + wid) * kFastBlockCap;
+    for (;;) {
+        uint32_t tile = 0;
+        if (lane == 0) tile = tile0 + atomicAdd(tileQueue, 1u);
+        tile = __shfl_sync(kFull, tile, 0);
+        if (tile >= tile1) break;
+        trace_tile<O>(t, cam, tp, fb, g, stats, s, prm, lane, tile);
+        __syncwarp();
     }
 }
 
@@ -287,54 +323,82 @@ __global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* cou
     }
 }
 
-// gradient_normal (tracer.cpp:285-294) with eval_full (traversal.cpp:126-141)
-// at p +- h e_axis, h = max(1e-3, 1e-4 t), for every queued pixel; one warp
-// per pixel.  Phase 1: the 32 lanes evaluate all primitives at the 6 taps
-// (independent work) into the warp's scratch.  Phase 2: lanes 0..5 run the
-// post-order operator program over those values (the same op order as the
-// reference walk, so exact mode stays bit-identical).
+// gradient_normal (tracer.cpp:285-294): eval_full (traversal.cpp:126-141) at
+// p +- h e_axis, h = max(1e-3, 1e-4 t).  One CTA per queued pixel:
+//   phase 1  every (frontier subtree, tap) pair is evaluated by one thread
+//            (post-order over <= 32 nodes) -- independent work;
+//   phase 2  six threads run the upper operator program over those values.
+// Each node still combines exactly the same operands in the same order as
+// the reference's serial walk, so the exact variant stays bit-identical.
 template <class O>
-__global__ void __launch_bounds__(128) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
+__device__ __forceinline__ float eval_subtree(const DevTree& t, uint2 range, F3 p) {
+    float stk[kFrontierMax / 2 + 1];
+    int sp = 0;
+    for (uint32_t j = range.x; j <= range.y; ++j) {
+        const uint32_t e = __ldg(&t.fullProgram[j]);
+        const uint32_t code = (e >> 26) & 0x1Fu;
+        const float4* P4 = t.words + (e & kSentinel) + 1;
+        if (e >> 31) {
+            float P[20];
+            load_params<5>(P, P4);
+            stk[sp++] = eval_primitive<O>(code, P, p);
+        } else {
+            float kd[2] = {0.f, 0.f};
+            if (code >= 6u) {
+                const float4 q = __ldg(P4);
+                kd[0] = q.x;
+                kd[1] = q.y;
+            }
+            const float right = stk[sp - 1], left = stk[sp - 2];
+            stk[sp - 2] = eval_operator<O>(code, kd, left, right);
+            --sp;
+        }
+    }
+    return stk[0];
+}
+
+template <class O>
+__global__ void __launch_bounds__(256) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
                                                   const uint32_t* counters, uint64_t* stats, float* scratch,
-                                                  uint32_t scratchWarps) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = min((gridDim.x * blockDim.x) >> 5, scratchWarps);
+                                                  uint32_t useSmem) {
+    extern __shared__ float dyn[];
+    __shared__ float res[6];
     const uint32_t n = counters[kCntFallback];
     if (threadIdx.x == 0 && blockIdx.x == 0)
         atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
-    if (warp >= nwarps) return;
-    float* sv = scratch + (size_t)warp * t.nprims * 6;
-    for (uint32_t i = warp; i < n; i += nwarps) {
+    float* vals = useSmem ? dyn : scratch + (size_t)blockIdx.x * t.nFrontier * 6;
+    // the serial upper program is staged once into shared memory (its loads
+    // would otherwise sit on the dependent chain of phase 2)
+    const uint32_t* upper = t.upperProgram;
+    if (useSmem && n > blockIdx.x) {
+        uint32_t* su = reinterpret_cast<uint32_t*>(dyn + t.nFrontier * 6);
+        for (uint32_t j = threadIdx.x; j < t.nUpper; j += blockDim.x) su[j] = __ldg(&t.upperProgram[j]);
+        upper = su;
+        __syncthreads();
+    }
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         const uint32_t p = g.fallback[i];
         const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
         const F3 pc = position_at(cam, fb, g, x, y);
         const float h = smax(1e-3f, E::mul(1e-4f, g.depth[p]));
-        const F3 taps[6] = {{E::add(pc.x, h), pc.y, pc.z}, {E::sub(pc.x, h), pc.y, pc.z},
-                            {pc.x, E::add(pc.y, h), pc.z}, {pc.x, E::sub(pc.y, h), pc.z},
-                            {pc.x, pc.y, E::add(pc.z, h)}, {pc.x, pc.y, E::sub(pc.z, h)}};
-        for (uint32_t k = lane; k < t.nprims * 6u; k += 32) {
-            const uint32_t prim = k / 6u, tap = k - prim * 6u;
-            const uint32_t w = __ldg(&t.primWords[prim]);
-            float P[20];
-            load_params<5>(P, t.words + w + 1);
-            F3 q = taps[0];
-#pragma unroll
-            for (int j = 1; j < 6; ++j)
-                if (tap == (uint32_t)j) q = taps[j];
-            sv[k] = eval_primitive<O>(blob_op(tree_blob(t.words, w)), P, q);
+        for (uint32_t k = threadIdx.x; k < t.nFrontier * 6u; k += blockDim.x) {
+            const uint32_t f = k / 6u, tap = k - f * 6u;
+            F3 q = pc;
+            const float dlt = (tap & 1u) ? E::sub(tap < 2u ? pc.x : tap < 4u ? pc.y : pc.z, h)
+                                         : E::add(tap < 2u ? pc.x : tap < 4u ? pc.y : pc.z, h);
+            if (tap < 2u) q.x = dlt;
+            else if (tap < 4u) q.y = dlt;
+            else q.z = dlt;
+            vals[k] = eval_subtree<O>(t, __ldg(&t.frontier[f]), q);
         }
-        __syncwarp();
-        float v = 0.0f;
-        if (lane < 6) {
+        __syncthreads();
+        if (threadIdx.x < 6) {
             float stk[kFullStackCap];
             int sp = 0;
-            uint32_t prim = 0;
-            for (uint32_t j = 0; j < t.nnodes; ++j) {
-                const uint32_t e = __ldg(&t.fullProgram[j]);
+            for (uint32_t j = 0; j < t.nUpper; ++j) {
+                const uint32_t e = upper[j];
                 if (e >> 31) {
-                    stk[sp++] = sv[prim * 6u + lane];
-                    ++prim;
+                    stk[sp++] = vals[(e & 0x7FFFFFFFu) * 6u + threadIdx.x];
                 } else {
                     const uint32_t code = (e >> 26) & 0x1Fu;
                     float kd[2] = {0.f, 0.f};
@@ -348,19 +412,17 @@ __global__ void __launch_bounds__(128) k_gradient(DevTree t, Cam cam, FrameBufs 
                     --sp;
                 }
             }
-            v = stk[0];
+            res[threadIdx.x] = stk[0];
         }
-        float f[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) f[k] = __shfl_sync(kFull, v, k);
-        if (lane == 0) {
-            const F3 dv{E::sub(f[0], f[1]), E::sub(f[2], f[3]), E::sub(f[4], f[5])};
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const F3 dv{E::sub(res[0], res[1]), E::sub(res[2], res[3]), E::sub(res[4], res[5])};
             const F3 nn = vnormalize<E>(dv);
             g.normal[3 * p + 0] = nn.x;
             g.normal[3 * p + 1] = nn.y;
             g.normal[3 * p + 2] = nn.z;
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -399,24 +461,35 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
 
 // ---------------------------------------------------------------- launchers
 
-void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
-                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
-                  uint32_t tile0, uint32_t tile1) {
-    if (tile1 <= tile0) return;
-    const uint32_t n = tile1 - tile0;
-    const size_t smem = sizeof(WarpSmem) * kTraceWarps;
-    const uint32_t blocks = (n + kTraceWarps - 1) / kTraceWarps;
-    static bool attrSet = false;
-    if (!attrSet) {
+uint32_t trace_grid_blocks(int smCount) {
+    static int perSM = 0;
+    if (perSM == 0) {
+        const size_t smem = sizeof(WarpSmem) * kTraceWarps;
         cudaFuncSetAttribute(k_trace<ExactOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_trace<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attrSet = true;
+        int a = 0, b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_trace<ExactOps>, kTraceWarps * 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace<FastOps>, kTraceWarps * 32, smem);
+        perSM = std::max(1, std::max(a, b));
     }
-    if (exact) {
-        k_trace<ExactOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1);
-    } else {
-        k_trace<FastOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1);
-    }
+    return (uint32_t)(perSM * smCount);
+}
+
+size_t trace_scratch_float4s(int smCount) { return (size_t)trace_grid_blocks(smCount) * kTraceWarps * kFastBlockCap; }
+
+void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
+                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
+                  uint32_t tile0, uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue) {
+    if (tile1 <= tile0) return;
+    const size_t smem = sizeof(WarpSmem) * kTraceWarps;
+    const uint32_t blocks = std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
+    cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
+    if (exact)
+        k_trace<ExactOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1, fastScratch,
+                                                                  tileQueue);
+    else
+        k_trace<FastOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1, fastScratch,
+                                                                 tileQueue);
 }
 
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
@@ -425,11 +498,19 @@ void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& ca
     cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
     dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
     k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
-    const uint32_t blocks = (scratchWarps + 3) / 4;
+    const size_t bytes = (size_t)t.nFrontier * 6 * sizeof(float) + (size_t)t.nUpper * sizeof(uint32_t);
+    const uint32_t useSmem = bytes <= kGradSmemBytes ? 1u : 0u;
+    const size_t smem = useSmem ? bytes : 0;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gradient<ExactOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemBytes);
+        cudaFuncSetAttribute(k_gradient<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemBytes);
+        attr = true;
+    }
     if (exact)
-        k_gradient<ExactOps><<<blocks, 128, 0, st>>>(t, cam, fb, g, counters, stats, scratch, scratchWarps);
+        k_gradient<ExactOps><<<scratchWarps, 256, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
     else
-        k_gradient<FastOps><<<blocks, 128, 0, st>>>(t, cam, fb, g, counters, stats, scratch, scratchWarps);
+        k_gradient<FastOps><<<scratchWarps, 256, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
 }
 
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
