@@ -283,7 +283,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "work": f"{flops_per_frame / 1e9:.3f} GFLOP/frame algorithmic (SURVEY.md appendix B), "
                 f"{st.fieldEvals} field evals/frame",
     }
-    result["frame_stats"] = {"fieldEvals": st.fieldEvals, "fragments": st.fragments,
+    result["frame_stats"] = {"fieldEvals": st.fieldEvals, "warpSteps": st.warpSteps,
+                             "laneUtilisation": round(st.fieldEvals / max(1, 32 * st.warpSteps), 4),
+                             "fragments": st.fragments,
                              "candidatePairs": st.candidatePairs, "maxOverlap": st.maxOverlap,
                              "normalFallbacks": st.normalFallbacks, "tileErrors": st.tileErrors}
 

@@ -119,6 +119,8 @@ typedef struct bt_stats {
     uint64_t candidatePairs;  /* (volume, tile) pairs ray-tested             */
     uint64_t tileErrors;      /* tiles flagged by the tracer                 */
     uint64_t normalFallbacks; /* pixels that took the 6-tap gradient path    */
+    uint64_t warpSteps;       /* lockstep march iterations of k_trace; lane
+                                 utilisation = fieldEvals / (32 * warpSteps) */
 } bt_stats;
 
 /* Device pointers of the context's G-buffer (for zero-copy gathers). */

@@ -53,7 +53,7 @@ class bt_stats(C.Structure):
                 ("primitiveEvals", C.c_uint64), ("treeNodeCount", C.c_uint64),
                 ("maxOverlap", C.c_uint32), ("maxCacheBytes", C.c_uint32), ("fieldFlops", C.c_uint64),
                 ("fragments", C.c_uint64), ("candidatePairs", C.c_uint64), ("tileErrors", C.c_uint64),
-                ("normalFallbacks", C.c_uint64)]
+                ("normalFallbacks", C.c_uint64), ("warpSteps", C.c_uint64)]
 
 
 class bt_gbuffer_view(C.Structure):

@@ -75,6 +75,7 @@ enum : int {
     kStMaxCache,
     kStTileErrors,
     kStFallbacks,
+    kStWarpSteps,  // lockstep march iterations (x32 lanes = evaluation slots offered)
     kStSlots
 };
 

@@ -107,7 +107,7 @@ BT_DEV float f_ellipsoid(float4 e, float4 f, F3 l) {  // k0 (k0 - 1) / k1
     const float bx = l.x * f.x, by = l.y * f.y, bz = l.z * f.z;
     const float k0 = fsqrt(ax * ax + ay * ay + az * az);
     const float k1 = fsqrt(bx * bx + by * by + bz * bz);
-    return k1 <= 0.0f ? e.w : __fdividef(k0 * (k0 - 1.0f), k1);
+    return k1 <= 0.0f ? e.w : k0 * (k0 - 1.0f) * FastOps::rcp(k1);
 }
 BT_DEV float f_cone(float4 e, float4 f, F3 l) {
     const float qx = fsqrt(l.x * l.x + l.z * l.z), qy = l.y;
@@ -128,7 +128,7 @@ BT_DEV float f_quadric(float4 e, float4 g, float4 h, F3 l) {  // f0 / max(|grad 
     const float gy = vv + e.y * y + e.w * x;
     const float gz = w + e.z * z + g.x * x + g.y * y;
     const float f0 = x * u + y * vv + z * w + h.y;
-    return __fdividef(f0, fmaxf(fsqrt(gx * gx + gy * gy + gz * gz), 1e-4f));
+    return f0 * FastOps::rcp(fmaxf(fsqrt(gx * gx + gy * gy + gz * gz), 1e-4f));
 }
 
 // One primitive at NP points; the parameter block is loaded once.
@@ -137,7 +137,7 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
     if (kind == 0u) {
         const float4 c = B[0];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(f_sphere(c, p[i]));
+        for (int i = 0; i < NP; ++i) v[i] = f_sphere(c, p[i]);
         return;
     }
     const float4 r0 = B[0], r1 = B[1], r2 = B[2], e = B[3];
@@ -163,8 +163,8 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_quadric(e, g, h, l[i]);
     }
-#pragma unroll
-    for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(v[i]);
+    // no NaN filter needed here: with finite points and validated parameters
+    // none of these closed forms produces NaN (the reference filters to 0)
 }
 
 BT_DEV float fast_disp(float a, float b, float k, float k6, float invk) {
@@ -183,12 +183,8 @@ BT_DEV float fast_smooth(uint32_t fl, float f0, float f1, float k, float k6, flo
     return is_nan(v) ? 0.0f : v;
 }
 
-BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
-    if (code <= 2u) return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
-    const uint32_t fl = op_flavour(code);
-    if (code <= 5u) return csg_op(fl, f0, f1);
+BT_DEV float fast_compact(uint32_t fl, const float4* B, float f0, float f1) {
     const float4 b0 = B[0];
-    if (code <= 8u) return fast_smooth(fl, f0, f1, b0.x, b0.y, b0.z);
     const float k = b0.x, d = b0.y;
     if (f0 > d || f1 > d) return csg_op(fl, f0, f1);
     const float g = fast_smooth(fl, f0, f1, k, b0.z, b0.w);
@@ -196,7 +192,25 @@ BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
     float br = k * smax(1.0f - x * B[1].x, 0.0f);
     br = is_nan(br) ? 0.0f : br;
     const float kp = fl == 0u ? br : smin(br, k);
-    return fast_smooth(fl, f0, f1, kp, kp * (1.0f / 6.0f), __fdividef(1.0f, kp));
+    return fast_smooth(fl, f0, f1, kp, kp * (1.0f / 6.0f), FastOps::rcp(kp));
+}
+
+BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
+    switch (code) {
+        case 0u: return f_inf();
+        case 1u: return f1;
+        case 2u: return f0;
+        case 3u: return smin(f0, f1);
+        case 4u: return smax(f0, f1);
+        case 5u: return smax(f0, -f1);
+        case 6u:
+        case 7u:
+        case 8u: {
+            const float4 b0 = B[0];
+            return fast_smooth(code - 6u, f0, f1, b0.x, b0.y, b0.z);
+        }
+        default: return fast_compact(code - 9u, B, f0, f1);
+    }
 }
 
 // Algorithm 3 over the fast blocks (`prm` = this warp's block area), at NP
@@ -207,8 +221,8 @@ BT_DEV void eval_view_fast(const WarpSmem& s, const float4* prm, const F3* p, fl
     uint32_t sp = 0;
     const uint32_t n = s.nView;
     for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t b = s.vBlob[i];
-        const float4* B = prm + s.vOff[i];
+        const uint32_t b = s.vHdr[i];
+        const float4* B = prm + (b & 0xFFFFu);
         if (blob_is_prim(b)) {
             float v[NP];
             fast_primitive<NP>(blob_op(b), B, p, v);

@@ -65,7 +65,7 @@ struct WarpSmem {
     // pruned view: blob (op possibly rewritten) and the source word of params
     uint32_t vBlob[kViewCap];
     uint32_t vWord[kViewCap];
-    uint16_t vOff[kViewCap];  // float4 offset of the node's fast parameter block
+    uint32_t vHdr[kViewCap];  // fast path: isPrim(1) op(5) | float4 offset of the parameter block
     // view-build traversal stack
     uint32_t sBlob[kStackCap];
     uint8_t sUse[kStackCap];
@@ -171,7 +171,7 @@ BT_DEV void view_append(WarpSmem& s, uint32_t blob, uint32_t word, bool copyPara
     if (floats > 0u && s.cacheFloats + floats <= kCacheFloats) s.cacheFloats += floats;
     s.vBlob[s.nView] = blob;
     s.vWord[s.nView] = word;
-    s.vOff[s.nView] = (uint16_t)s.vEnd;
+    s.vHdr[s.nView] = (blob & 0xFC000000u) | s.vEnd;
     s.vEnd += fast_block_size(blob);
     s.nView++;
 }
@@ -321,42 +321,49 @@ BT_DEV float eval_view(const WarpSmem& s, const float4* words, F3 p) {
 // 1 needs f(t0), 2 needs f(tn) (main step), 3 needs f(tb) (unrelaxed
 // back-off after an overshoot).  March arithmetic is always exact.
 
+// Compact march state: 6 floats + 2 words per ray (register pressure is
+// what limits the trace kernel's occupancy).  `st` packs the phase and the
+// flags; on completion `t` holds the hit position.  r = f / L is recomputed
+// where the reference reuses it (f is unchanged in between, same bits).
+constexpr uint32_t kPhaseMask = 3u;  // 0 done, 1 needs f(t0), 2 needs f(tn), 3 needs f(tb)
+constexpr uint32_t kRelax = 4u, kSaved = 8u, kHitFlag = 16u, kSlot1 = 32u;
+
 struct March {
-    float t, f, r, tn, t1, savedT, savedF, evalT;
-    uint32_t phase;
-    bool relaxOn, savedValid, hit;
-    float hitT;
-    uint32_t evals;
+    float t, f, t1, savedT, savedF, evalT;
+    uint32_t st, evals;
 };
 
+BT_DEV uint32_t march_phase(const March& m) { return m.st & kPhaseMask; }
+BT_DEV bool march_hit(const March& m) { return (m.st & kHitFlag) != 0u; }
+
 BT_DEV void march_finish(March& m, bool hit, float t) {
-    m.phase = 0;
-    m.hit = hit;
-    m.hitT = t;
+    m.st = (m.st & kSlot1) | (hit ? kHitFlag : 0u);
+    m.t = t;
 }
+
+BT_DEV void march_set_phase(March& m, uint32_t ph) { m.st = (m.st & ~kPhaseMask) | ph; }
 
 // Advance without evaluating until a field value is needed (reference loop
 // head: step computation, saved-sphere reuse, clamp to t1).
 BT_DEV void march_advance(March& m, const TraceParams& tp) {
     for (;;) {
-        m.r = E::mul(m.f, tp.invL);
-        if (!is_finite(m.r)) {
+        const float r = E::mul(m.f, tp.invL);
+        if (!is_finite(r)) {
             march_finish(m, false, 0.0f);
             return;
         }
-        float step = m.relaxOn ? E::mul(tp.relax, m.r) : m.r;
+        float step = (m.st & kRelax) ? E::mul(tp.relax, r) : r;
         step = smax(step, tp.minStep);
         float tn = E::add(m.t, step);
         bool reused = false;
         float fn = 0.0f;
-        if (m.savedValid && tn >= m.savedT) {
+        if ((m.st & kSaved) && tn >= m.savedT) {
             if (m.savedT >= E::add(m.t, tp.minStep) && m.savedT <= m.t1) {
                 tn = m.savedT;
                 fn = m.savedF;
                 reused = true;
             }
-            m.savedValid = false;
-            m.relaxOn = true;
+            m.st = (m.st & ~kSaved) | kRelax;
         }
         if (tn > m.t1) {
             if (m.t >= m.t1) {
@@ -367,9 +374,8 @@ BT_DEV void march_advance(March& m, const TraceParams& tp) {
             reused = false;
         }
         if (!reused) {
-            m.tn = tn;
             m.evalT = tn;
-            m.phase = 2;
+            march_set_phase(m, 2u);
             return;
         }
         // reused sample: never an overshoot
@@ -386,91 +392,69 @@ BT_DEV void march_advance(March& m, const TraceParams& tp) {
     }
 }
 
-BT_DEV void march_idle(March& m) {
-    m.phase = 0;
+BT_DEV void march_idle(March& m, uint32_t slot) {
+    m.st = slot ? kSlot1 : 0u;
     m.evals = 0;
-    m.hit = false;
-    m.hitT = 0.0f;
+    m.t = 0.0f;
 }
 
-BT_DEV void march_begin(March& m, float t0, float t1) {
+BT_DEV void march_begin(March& m, float t0, float t1, uint32_t slot) {
     m.evals = 0;
-    m.hit = false;
-    m.hitT = 0.0f;
-    m.relaxOn = true;
-    m.savedValid = false;
+    m.st = (slot ? kSlot1 : 0u) | kRelax;
     m.t1 = t1;
     if (t0 > t1) {
-        m.phase = 0;
+        march_finish(m, false, 0.0f);
         return;
     }
     m.t = t0;
     m.evalT = t0;
-    m.phase = 1;
+    march_set_phase(m, 1u);
 }
 
+// One field value consumed (tracer.hpp:115-175).  Every path that continues
+// the march funnels into a single march_advance call site, which keeps the
+// divergent parts of a warp step short.
 BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     m.evals++;
-    if (m.phase == 1) {
-        m.f = v;
-        if (m.f <= tp.hitEps) {
-            march_finish(m, true, m.t);
-            return;
-        }
-        march_advance(m, tp);
-        return;
-    }
-    if (m.phase == 3) {
+    bool advance = false;
+    if (march_phase(m) != 2u) {  // start sample or back-off sample: the march moves to it
         m.t = m.evalT;
         m.f = v;
-        if (m.f <= tp.hitEps) {
-            march_finish(m, true, m.t);
-            return;
-        }
-        march_advance(m, tp);
-        return;
-    }
-    // phase 2: main step at tn
-    const float fn = v, tn = m.tn;
-    const bool overshoot = m.relaxOn && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(fn)) ||
-                                         fn < -tp.hitEps);
-    if (overshoot) {
-        m.savedT = tn;
-        m.savedF = fn;
-        m.savedValid = true;
-        m.relaxOn = false;
-        const float tb = E::add(m.t, smax(m.r, tp.minStep));
-        if (tb >= m.savedT) {
-            m.t = m.savedT;
-            m.f = m.savedF;
-            m.savedValid = false;
-            m.relaxOn = true;
-        } else if (tb > m.t1) {
-            march_finish(m, false, 0.0f);
-            return;
+        if (m.f <= tp.hitEps) march_finish(m, true, m.t);
+        else advance = true;
+    } else {
+        const float fn = v, tn = m.evalT;
+        const bool overshoot = (m.st & kRelax) && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(fn)) ||
+                                                   fn < -tp.hitEps);
+        if (!overshoot) {
+            if (fn <= tp.hitEps) march_finish(m, true, tn);
+            else if (tn >= m.t1) march_finish(m, false, 0.0f);
+            else {
+                m.t = tn;
+                m.f = fn;
+                advance = true;
+            }
         } else {
-            m.evalT = tb;
-            m.phase = 3;
-            return;
+            // remember the non-overlapping sphere, back off to the safe one
+            m.savedT = tn;
+            m.savedF = fn;
+            m.st = (m.st & ~kRelax) | kSaved;
+            const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
+            if (tb >= m.savedT) {
+                m.t = m.savedT;
+                m.f = m.savedF;
+                m.st = (m.st & ~kSaved) | kRelax;
+                if (m.f <= tp.hitEps) march_finish(m, true, m.t);
+                else advance = true;
+            } else if (tb > m.t1) {
+                march_finish(m, false, 0.0f);
+            } else {
+                m.evalT = tb;
+                march_set_phase(m, 3u);
+            }
         }
-        if (m.f <= tp.hitEps) {
-            march_finish(m, true, m.t);
-            return;
-        }
-        march_advance(m, tp);
-        return;
     }
-    if (fn <= tp.hitEps) {
-        march_finish(m, true, tn);
-        return;
-    }
-    if (tn >= m.t1) {
-        march_finish(m, false, 0.0f);
-        return;
-    }
-    m.t = tn;
-    m.f = fn;
-    march_advance(m, tp);
+    if (advance) march_advance(m, tp);
 }
 
 }  // namespace btk

@@ -972,6 +972,7 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
     out->candidatePairs = cnt[kCntCandidates];
     out->tileErrors = st[kStTileErrors];
     out->normalFallbacks = st[kStFallbacks];
+    out->warpSteps = st[kStWarpSteps];
     if (c->haveAbuffer) {
         const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
         uint32_t total = 0;

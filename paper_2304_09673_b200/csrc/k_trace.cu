@@ -16,6 +16,7 @@
 // O = ExactOps gives bit-identical results to the CPU reference; O = FastOps
 // lets nvcc contract the field arithmetic into FFMA (tolerance path).
 #include <algorithm>
+#include <cstdlib>
 
 #include "bt_device.h"
 #include "bt_fast.cuh"
@@ -35,7 +36,6 @@ template <class O> __device__ __forceinline__ F3 ray_point(F3 o, F3 d, float t) 
 struct RayLane {
     March m;
     F3 dir;
-    uint32_t slot;
 };
 
 __device__ __forceinline__ void swap_lanes(RayLane& a, RayLane& b) {
@@ -82,6 +82,7 @@ __device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, con
 
     uint32_t tileMaxOv = 0, tileCache = 0, tileErr = 0;
     uint64_t stFE = 0, stRNV = 0, stPE = 0, stFL = 0;
+    uint32_t warpSteps = 0;
 
     if (cnt != 0) {
         F3 dir[2];
@@ -131,7 +132,7 @@ __device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, con
             }
             if (IsFast<O>::value) {  // lane-parallel parameter-block conversion
                 for (uint32_t i = lane; i < s.nView; i += 32)
-                    convert_node(s.vBlob[i], t.words + s.vWord[i] + 1, prm + s.vOff[i]);
+                    convert_node(s.vBlob[i], t.words + s.vWord[i] + 1, prm + (s.vHdr[i] & 0xFFFFu));
                 __syncwarp();
             }
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
@@ -140,30 +141,28 @@ __device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, con
             // field once per lane (one instantiation of the evaluator keeps the
             // hot loop inside the instruction cache).
             RayLane cur, oth;
-            cur.slot = 0;
-            oth.slot = 1;
             cur.dir = dir[0];
             oth.dir = dir[1];
-            if (!found[0]) march_begin(cur.m, E::div(vz0, ddf[0]), E::div(vz1, ddf[0]));
-            else march_idle(cur.m);
-            if (!found[1]) march_begin(oth.m, E::div(vz0, ddf[1]), E::div(vz1, ddf[1]));
-            else march_idle(oth.m);
-            if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
-            // (evaluating both slots in one pass was measured slower: as soon as
-            // one lane has two live rays the whole warp pays two evaluations)
-            while (__any_sync(kFull, cur.m.phase != 0)) {
+            if (!found[0]) march_begin(cur.m, E::div(vz0, ddf[0]), E::div(vz1, ddf[0]), 0u);
+            else march_idle(cur.m, 0u);
+            if (!found[1]) march_begin(oth.m, E::div(vz0, ddf[1]), E::div(vz1, ddf[1]), 1u);
+            else march_idle(oth.m, 1u);
+            if (march_phase(cur.m) == 0u && march_phase(oth.m) != 0u) swap_lanes(cur, oth);
+            while (__any_sync(kFull, march_phase(cur.m) != 0u)) {
+                ++warpSteps;
                 const F3 p = ray_point<O>(cam.pos, cur.dir, cur.m.evalT);
                 float v;
                 if (IsFast<O>::value) eval_view_fast<1>(s, prm, &p, &v);
                 else v = eval_view<O>(s, t.words, p);
-                if (cur.m.phase != 0) {
+                if (march_phase(cur.m) != 0u) {
                     march_consume(cur.m, v, tp);
-                    if (cur.m.phase == 0 && oth.m.phase != 0) swap_lanes(cur, oth);
+                    if (march_phase(cur.m) == 0u && march_phase(oth.m) != 0u) swap_lanes(cur, oth);
                 }
             }
             const uint32_t nView = s.nView, nPrim = s.nPrim, fl = s.flops;
-            const March& m0 = cur.slot == 0 ? cur.m : oth.m;
-            const March& m1 = cur.slot == 0 ? oth.m : cur.m;
+            const bool curIs0 = (cur.m.st & kSlot1) == 0u;
+            const March& m0 = curIs0 ? cur.m : oth.m;
+            const March& m1 = curIs0 ? oth.m : cur.m;
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const March& mj = j == 0 ? m0 : m1;
@@ -174,10 +173,10 @@ __device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, con
                 stRNV += (uint64_t)e * nView;
                 stPE += (uint64_t)e * nPrim;
                 stFL += (uint64_t)e * fl;
-                if (mj.hit) {
+                if (march_hit(mj)) {
                     found[j] = true;
                     hitf[j] = true;
-                    depth[j] = mj.hitT;
+                    depth[j] = mj.t;
                 }
             }
             __syncwarp();
@@ -209,14 +208,15 @@ __device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, con
         if (tileMaxOv) atomicMax((unsigned long long*)&stats[kStMaxOverlap], (unsigned long long)tileMaxOv);
         if (tileCache) atomicMax((unsigned long long*)&stats[kStMaxCache], (unsigned long long)tileCache);
         if (tileErr) atomicAdd((unsigned long long*)&stats[kStTileErrors], 1ull);
+        if (warpSteps) atomicAdd((unsigned long long*)&stats[kStWarpSteps], (unsigned long long)warpSteps);
     }
 }
 
 // Persistent kernel: each warp pulls tiles from a queue (tiles differ wildly
 // in cost -- empty tiles exit at once) and owns a fixed slot of the fast
 // parameter-block scratch.
-template <class O>
-__global__ void __launch_bounds__(kTraceWarps * 32, 8) k_trace(DevTree t, Cam cam, TraceParams tp, FrameBufs fb,
+template <class O, int MinBlocks>
+__global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks) k_trace(DevTree t, Cam cam, TraceParams tp, FrameBufs fb,
                                                             GBuf g, uint64_t* stats, uint32_t tile0, uint32_t tile1,
                                                             float4* fastScratch, uint32_t* tileQueue) {
     extern __shared__ __align__(16) unsigned char smemRaw[];
@@ -330,9 +330,11 @@ __global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* cou
 //   phase 2  six threads run the upper operator program over those values.
 // Each node still combines exactly the same operands in the same order as
 // the reference's serial walk, so the exact variant stays bit-identical.
+// One frontier subtree at the 6 gradient taps: parameters are loaded once per
+// node and the 6 evaluations are independent (ILP).
 template <class O>
-__device__ __forceinline__ float eval_subtree(const DevTree& t, uint2 range, F3 p) {
-    float stk[kFrontierMax / 2 + 1];
+__device__ __forceinline__ void eval_subtree6(const DevTree& t, uint2 range, const F3* taps, float* out) {
+    float stk[6][kFrontierMax / 2 + 1];
     int sp = 0;
     for (uint32_t j = range.x; j <= range.y; ++j) {
         const uint32_t e = __ldg(&t.fullProgram[j]);
@@ -341,7 +343,9 @@ __device__ __forceinline__ float eval_subtree(const DevTree& t, uint2 range, F3 
         if (e >> 31) {
             float P[20];
             load_params<5>(P, P4);
-            stk[sp++] = eval_primitive<O>(code, P, p);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) stk[k][sp] = eval_primitive<O>(code, P, taps[k]);
+            ++sp;
         } else {
             float kd[2] = {0.f, 0.f};
             if (code >= 6u) {
@@ -349,12 +353,13 @@ __device__ __forceinline__ float eval_subtree(const DevTree& t, uint2 range, F3 
                 kd[0] = q.x;
                 kd[1] = q.y;
             }
-            const float right = stk[sp - 1], left = stk[sp - 2];
-            stk[sp - 2] = eval_operator<O>(code, kd, left, right);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) stk[k][sp - 2] = eval_operator<O>(code, kd, stk[k][sp - 2], stk[k][sp - 1]);
             --sp;
         }
     }
-    return stk[0];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[k] = stk[k][0];
 }
 
 template <class O>
@@ -381,15 +386,14 @@ __global__ void __launch_bounds__(256) k_gradient(DevTree t, Cam cam, FrameBufs 
         const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
         const F3 pc = position_at(cam, fb, g, x, y);
         const float h = smax(1e-3f, E::mul(1e-4f, g.depth[p]));
-        for (uint32_t k = threadIdx.x; k < t.nFrontier * 6u; k += blockDim.x) {
-            const uint32_t f = k / 6u, tap = k - f * 6u;
-            F3 q = pc;
-            const float dlt = (tap & 1u) ? E::sub(tap < 2u ? pc.x : tap < 4u ? pc.y : pc.z, h)
-                                         : E::add(tap < 2u ? pc.x : tap < 4u ? pc.y : pc.z, h);
-            if (tap < 2u) q.x = dlt;
-            else if (tap < 4u) q.y = dlt;
-            else q.z = dlt;
-            vals[k] = eval_subtree<O>(t, __ldg(&t.frontier[f]), q);
+        const F3 taps[6] = {{E::add(pc.x, h), pc.y, pc.z}, {E::sub(pc.x, h), pc.y, pc.z},
+                            {pc.x, E::add(pc.y, h), pc.z}, {pc.x, E::sub(pc.y, h), pc.z},
+                            {pc.x, pc.y, E::add(pc.z, h)}, {pc.x, pc.y, E::sub(pc.z, h)}};
+        for (uint32_t f = threadIdx.x; f < t.nFrontier; f += blockDim.x) {
+            float v6[6];
+            eval_subtree6<O>(t, __ldg(&t.frontier[f]), taps, v6);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) vals[f * 6u + k] = v6[k];
         }
         __syncthreads();
         if (threadIdx.x < 6) {
@@ -438,13 +442,13 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
         const float4 r = fb.rays[(size_t)tile * 64 + ((y & 7) << 3) + (x & 7)];
         const F3 d{r.x, r.y, r.z};
         March m;
-        march_begin(m, E::div(cam.nearZ, r.w), E::div(cam.farZ, r.w));
-        while (m.phase != 0) {
+        march_begin(m, E::div(cam.nearZ, r.w), E::div(cam.farZ, r.w), 0u);
+        while (march_phase(m) != 0u) {
             const float v = eval_full<O>(t, ray_point<O>(cam.pos, d, m.evalT));
             march_consume(m, v, tp);
         }
-        g.hit[p] = m.hit ? 1 : 0;
-        g.depth[p] = m.hit ? m.hitT : 0.0f;
+        g.hit[p] = march_hit(m) ? 1 : 0;
+        g.depth[p] = march_hit(m) ? m.t : 0.0f;
         g.evalCount[p] = m.evals;
         fe = m.evals;
     }
@@ -461,21 +465,59 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
 
 // ---------------------------------------------------------------- launchers
 
+// Register budget of the FMA-path kernel (blocks of 4 warps per SM the
+// compiler must fit): a compile-time variant selected once per process
+// ($BT_TRACE_MINBLOCKS, default kDefaultMinBlocks) so the budget can be swept
+// on the device without rebuilding.
+constexpr int kDefaultMinBlocks = 5;  // measured best of {4,5,6,8} on C3
+
+template <int MB> struct TraceVariant {
+    static void* fn(bool exact) {
+        return exact ? (void*)k_trace<ExactOps, MB> : (void*)k_trace<FastOps, MB>;
+    }
+};
+
+int trace_min_blocks() {
+    static int mb = 0;
+    if (mb == 0) {
+        mb = kDefaultMinBlocks;
+        if (const char* e = getenv("BT_TRACE_MINBLOCKS")) {
+            const int v = atoi(e);
+            if (v == 4 || v == 5 || v == 6 || v == 8) mb = v;
+        }
+    }
+    return mb;
+}
+
+void* trace_fn(bool exact) {
+    switch (trace_min_blocks()) {
+        case 4: return TraceVariant<4>::fn(exact);
+        case 5: return TraceVariant<5>::fn(exact);
+        case 6: return TraceVariant<6>::fn(exact);
+        default: return TraceVariant<8>::fn(exact);
+    }
+}
+
 uint32_t trace_grid_blocks(int smCount) {
     static int perSM = 0;
     if (perSM == 0) {
         const size_t smem = sizeof(WarpSmem) * kTraceWarps;
-        cudaFuncSetAttribute(k_trace<ExactOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_trace<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int a = 0, b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_trace<ExactOps>, kTraceWarps * 32, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace<FastOps>, kTraceWarps * 32, smem);
-        perSM = std::max(1, std::max(a, b));
+        int best = 1;
+        for (int ex = 0; ex < 2; ++ex) {
+            const void* f = trace_fn(ex != 0);
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int a = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, f, kTraceWarps * 32, smem);
+            best = std::max(best, a);
+        }
+        perSM = best;
     }
     return (uint32_t)(perSM * smCount);
 }
 
-size_t trace_scratch_float4s(int smCount) { return (size_t)trace_grid_blocks(smCount) * kTraceWarps * kFastBlockCap; }
+size_t trace_scratch_float4s(int smCount) {
+    return (size_t)trace_grid_blocks(smCount) * kTraceWarps * kFastBlockCap + 8;
+}
 
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                   const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
@@ -484,12 +526,9 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
     const size_t smem = sizeof(WarpSmem) * kTraceWarps;
     const uint32_t blocks = std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
     cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
-    if (exact)
-        k_trace<ExactOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1, fastScratch,
-                                                                  tileQueue);
-    else
-        k_trace<FastOps><<<blocks, kTraceWarps * 32, smem, st>>>(t, cam, tp, fb, g, stats, tile0, tile1, fastScratch,
-                                                                 tileQueue);
+    void* args[] = {(void*)&t, (void*)&cam, (void*)&tp, (void*)&fb, (void*)&g, (void*)&stats,
+                    (void*)&tile0, (void*)&tile1, (void*)&fastScratch, (void*)&tileQueue};
+    cudaLaunchKernel(trace_fn(exact), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
 }
 
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
