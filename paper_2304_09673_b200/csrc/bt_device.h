@@ -27,6 +27,7 @@ struct DevTree {
     const uint2* frontier = nullptr;       // ordinal range [lo, hi] per subtree
     const uint32_t* upperProgram = nullptr;// bit31 ? load frontier value : (op<<26 | word)
     uint32_t nFrontier = 0, nUpper = 0;
+    uint32_t upperIsChain = 0;  // upper program = F0 (Fi op)*: left comb, register accumulator
 };
 constexpr uint32_t kFrontierMax = 32;
 constexpr size_t kGradSmemBytes = 160 * 1024;  // frontier values kept in shared memory up to this size

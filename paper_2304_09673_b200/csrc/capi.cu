@@ -82,7 +82,7 @@ struct bt_ctx {
     DevBuf<float4> words;
     DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram;
     DevBuf<uint2> frontier;
-    uint32_t nFrontier = 0, nUpper = 0;
+    uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0;
     DevBuf<int32_t> compactAnc;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
@@ -149,6 +149,7 @@ DevTree dev_tree(const bt_ctx* c) {
     t.upperProgram = c->upperProgram.ptr;
     t.nFrontier = c->nFrontier;
     t.nUpper = c->nUpper;
+    t.upperIsChain = c->upperIsChain;
     return t;
 }
 
@@ -566,6 +567,11 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->upperProgram.ptr, upper.data(), upper.size() * 4, cudaMemcpyHostToDevice, c->stream));
     c->nFrontier = (uint32_t)frontier.size();
     c->nUpper = (uint32_t)upper.size();
+    {  // left comb: LOAD, then (LOAD, OP) pairs -- every operator folds the running value with a fresh load
+        bool chain = !upper.empty() && (upper[0] >> 31) && (upper.size() % 2 == 1);
+        for (size_t j = 1; chain && j < upper.size(); j += 2) chain = (upper[j] >> 31) && !(upper[j + 1] >> 31);
+        c->upperIsChain = chain ? 1u : 0u;
+    }
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->nwords = nwords;
     c->nnodes = nnodes;
@@ -969,7 +975,7 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
     out->maxOverlap = (uint32_t)st[kStMaxOverlap];
     out->maxCacheBytes = (uint32_t)st[kStMaxCache];
     out->fieldFlops = st[kStFlops];
-    out->candidatePairs = cnt[kCntCandidates];
+    out->candidatePairs = cnt[kCntPool];
     out->tileErrors = st[kStTileErrors];
     out->normalFallbacks = st[kStFallbacks];
     out->warpSteps = st[kStWarpSteps];

@@ -5,7 +5,8 @@
 //   k_voi            volume of interest per primitive           (linear_tree.cpp:216-283)
 //   k_camera         pixel rays, tile cones, superblock cones   (camera.cpp:29-37, abuffer.cpp:117-149)
 //   k_pairs          (volume, superblock) coarse cull           (superset of abuffer.cpp:193-196)
-//   k_raster         exact tile cull + 64 pixel-ray intervals   (abuffer.cpp:188-222)
+//   k_tiles          exact tile cone + pixel pyramid per tile   (abuffer.cpp:193-196)
+//   k_raster         64 exact pixel-ray intervals per item      (abuffer.cpp:198-222)
 //   k_scan           tile counts -> CSR offsets (single pass)
 //   k_scatter        unsorted pool -> CSR slots
 //   k_sort           per-tile rank sort by (zEntry, word)       (insert_sorted, abuffer.cpp:166-173)
@@ -249,19 +250,19 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
     }
 }
 
-// one warp per (volume, superblock) pair, grid-stride.  Lanes test the 64
-// tiles' exact cones, then every surviving tile is swept by the warp: two
-// pixel rays per lane, exact interval + clip + NDC, warp min/max.
-__global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameBufs fb, int tilesX,
-                                                 int tilesY, uint32_t tile0, uint32_t tile1) {
+// One warp per (volume, superblock) pair, grid-stride: every lane tests two of
+// the superblock's 64 tiles with the exact reference cone (abuffer.cpp:193-196)
+// and the tile's pixel-centre pyramid; surviving (tile, volume) items are
+// appended with ONE warp-aggregated atomic per pair.
+__global__ void __launch_bounds__(256) k_tiles(Cam cam, const Voi* vois, FrameBufs fb, int tilesX, int tilesY,
+                                                uint32_t tile0, uint32_t tile1) {
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t npairs = min((uint64_t)fb.counters[kCntPairs], fb.pairCap);
     const int sbX = (tilesX + kSB - 1) / kSB;
     for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npairs; p += nwarps) {
         const uint2 pr = fb.pairs[p];
-        const Voi v = vois[pr.x];
-        const Sphere bs = bounding_sphere(v);
+        const Sphere bs = bounding_sphere(vois[pr.x]);
         const int sx = pr.y % sbX, sy = pr.y / sbX;
         bool pass[2];
         uint32_t tiles[2];
@@ -277,63 +278,85 @@ __global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameB
                 k.axis = F3{c.x, c.y, c.z};
                 k.cosH = c.w;
                 k.sinH = fb.coneSin[tiles[h]];
-                // exact reference cull (abuffer.cpp:193-196) and the pixel-centre
-                // pyramid (rays outside it cannot hit: skips empty ray sweeps)
                 pass[h] = cone_may_touch(k, cam.pos, bs) &&
                           pyramid_may_touch(fb.tileFrustum + (size_t)tiles[h] * 4, cam.pos, bs);
             }
         }
-        uint64_t mask = (uint64_t)__ballot_sync(kFull, pass[0]) | ((uint64_t)__ballot_sync(kFull, pass[1]) << 32);
-        if (mask == 0) continue;
-        if (lane == 0) atomicAdd(&fb.counters[kCntCandidates], (uint32_t)__popcll(mask));
-        // per-volume constants shared by every ray
+        const uint32_t m0 = __ballot_sync(kFull, pass[0]), m1 = __ballot_sync(kFull, pass[1]);
+        const uint32_t n = __popc(m0) + __popc(m1);
+        if (n == 0) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&fb.counters[kCntPool], n);
+        base = __shfl_sync(kFull, base, 0);
+        const uint32_t below = (1u << lane) - 1u;
+        if (pass[0]) {
+            const uint32_t slot = base + __popc(m0 & below);
+            if (slot < fb.poolCap) fb.pool[slot] = make_uint4(tiles[0], pr.x, 0u, 0u);
+        }
+        if (pass[1]) {
+            const uint32_t slot = base + __popc(m0) + __popc(m1 & below);
+            if (slot < fb.poolCap) fb.pool[slot] = make_uint4(tiles[1], pr.x, 0u, 0u);
+        }
+    }
+}
+
+constexpr uint32_t kNoFragment = 0xFFFFFFFFu;
+
+// One warp per (tile, volume) item, grid-stride: the tile's 64 pixel rays (two
+// per lane) are intersected with the volume exactly (abuffer.cpp:200-216),
+// clipped to [near, far], mapped to NDC and reduced with min/max (order-free
+// on these finite values).  The fragment lands in the item's own slot, so no
+// global append counter is contended; misses mark the slot empty.
+__global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameBufs fb) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nitems = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
+    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems; it += nwarps) {
+        const uint4 item = fb.pool[it];
+        const uint32_t tile = item.x;
+        const Voi v = vois[item.y];
+        const int tilesX = (cam.width + kTile - 1) / kTile;
+        const int tx = (int)(tile % (uint32_t)tilesX), ty = (int)(tile / (uint32_t)tilesX);
         F3 ol{0.f, 0.f, 0.f};
         if (v.family == 1u) ol = qrotate<E>(qconj(v.rot), vsub<E>(cam.pos, v.center));
-        while (mask) {
-            const int lt = __ffsll((long long)mask) - 1;
-            mask &= mask - 1;
-            const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
-            const uint32_t tile = (uint32_t)(ty * tilesX + tx);
-            float entry = f_inf(), exitv = -f_inf();
-            bool any = false;
+        float entry = f_inf(), exitv = -f_inf();
+        bool any = false;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int pix = lane + 32 * h;
-                const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
-                if (px >= cam.width || py >= cam.height) continue;
-                const float4 rd = fb.rays[(size_t)tile * 64 + pix];
-                const F3 d{rd.x, rd.y, rd.z};
-                float t0, t1;
-                bool hit;
-                if (v.family == 0u)
-                    hit = ray_sphere(cam.pos, d, v.center, v.radius, t0, t1);
-                else if (v.family == 1u)
-                    hit = ray_obb_local(ol, d, v.rot, v.half, t0, t1);
-                else
-                    hit = ray_capsule(cam.pos, d, v.center, v.axisEnd, v.radius, t0, t1);
-                if (!hit) continue;
-                float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
-                if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
-                vz0 = smax(vz0, cam.nearZ);
-                vz1 = smin(vz1, cam.farZ);
-                entry = smin(entry, ndc_from_view_z(cam, vz0));
-                exitv = smax(exitv, ndc_from_view_z(cam, vz1));
-                any = true;
-            }
-            if (!__any_sync(kFull, any)) continue;
+        for (int h = 0; h < 2; ++h) {
+            const int pix = lane + 32 * h;
+            const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
+            if (px >= cam.width || py >= cam.height) continue;
+            const float4 rd = fb.rays[(size_t)tile * 64 + pix];
+            const F3 d{rd.x, rd.y, rd.z};
+            float t0, t1;
+            bool hit;
+            if (v.family == 0u)
+                hit = ray_sphere(cam.pos, d, v.center, v.radius, t0, t1);
+            else if (v.family == 1u)
+                hit = ray_obb_local(ol, d, v.rot, v.half, t0, t1);
+            else
+                hit = ray_capsule(cam.pos, d, v.center, v.axisEnd, v.radius, t0, t1);
+            if (!hit) continue;
+            float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
+            if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
+            vz0 = smax(vz0, cam.nearZ);
+            vz1 = smin(vz1, cam.farZ);
+            entry = smin(entry, ndc_from_view_z(cam, vz0));
+            exitv = smax(exitv, ndc_from_view_z(cam, vz1));
+            any = true;
+        }
+        if (!__any_sync(kFull, any)) {
+            if (lane == 0) fb.pool[it].x = kNoFragment;
+            continue;
+        }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
-                exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
-            }
-            if (lane == 0) {
-                const uint32_t slot = atomicAdd(&fb.counters[kCntPool], 1u);
-                if (slot < fb.poolCap)
-                    fb.pool[slot] = make_uint4(tile, pr.x, __float_as_uint(entry), __float_as_uint(exitv));
-                else
-                    atomicExch(&fb.counters[kCntOverflow], 1u);
-                atomicAdd(&fb.tileCount[tile], 1u);
-            }
+        for (int o = 16; o > 0; o >>= 1) {
+            entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
+            exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
+        }
+        if (lane == 0) {
+            fb.pool[it] = make_uint4(tile, item.y, __float_as_uint(entry), __float_as_uint(exitv));
+            atomicAdd(&fb.tileCount[tile], 1u);
         }
     }
 }
@@ -415,6 +438,7 @@ __global__ void k_scatter(const Voi* vois, FrameBufs fb) {
     const uint32_t n = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint4 r = fb.pool[i];
+        if (r.x == kNoFragment) continue;
         const uint32_t slot = tile_offset(fb, r.x) + atomicAdd(&fb.tileCursor[r.x], 1u);
         fb.unsorted[slot] = make_uint4(vois[r.y].word, r.z, r.w, r.y);
     }
@@ -509,7 +533,8 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
     cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
     if (nvoi > 0) {
         k_pairs<<<(nvoi * 32 + 255) / 256, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1);
-        k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
+        k_tiles<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
+        k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb);
     }
     const uint32_t nblocks = (tiles + kScanBlock - 1) / kScanBlock;
     k_scan<<<nblocks, 1024, 0, st>>>(fb, tiles);

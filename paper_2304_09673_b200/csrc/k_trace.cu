@@ -396,7 +396,24 @@ __global__ void __launch_bounds__(256) k_gradient(DevTree t, Cam cam, FrameBufs 
             for (int k = 0; k < 6; ++k) vals[f * 6u + k] = v6[k];
         }
         __syncthreads();
-        if (threadIdx.x < 6) {
+        if (threadIdx.x < 6 && t.upperIsChain) {
+            // left comb: acc = F0; acc = op(acc, Fi) -- same operand order as the
+            // post-order walk, no stack traffic on the serial dependency chain
+            float acc = vals[(upper[0] & 0x7FFFFFFFu) * 6u + threadIdx.x];
+            for (uint32_t j = 1; j < t.nUpper; j += 2) {
+                const float right = vals[(upper[j] & 0x7FFFFFFFu) * 6u + threadIdx.x];
+                const uint32_t e = upper[j + 1];
+                const uint32_t code = (e >> 26) & 0x1Fu;
+                float kd[2] = {0.f, 0.f};
+                if (code >= 6u) {
+                    const float4 q = __ldg(t.words + (e & kSentinel) + 1);
+                    kd[0] = q.x;
+                    kd[1] = q.y;
+                }
+                acc = eval_operator<O>(code, kd, acc, right);
+            }
+            res[threadIdx.x] = acc;
+        } else if (threadIdx.x < 6) {
             float stk[kFullStackCap];
             int sp = 0;
             for (uint32_t j = 0; j < t.nUpper; ++j) {

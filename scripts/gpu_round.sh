@@ -9,4 +9,5 @@ timeout 400 python bench.py > gpurun_out/${TAG}_bench.txt 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-sweep > gpurun_out/${TAG}_ncu1.txt 2>&1
 timeout 500 ncu --set full --clock-control none --import-source on -k regex:k_trace -s 2 -c 1 -o gpurun_out/${TAG}_prof_trace python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-sweep > gpurun_out/${TAG}_ncu2.txt 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gradient -s 1 -c 1 -o gpurun_out/${TAG}_prof_grad python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-sweep > gpurun_out/${TAG}_ncu3.txt 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_raster -s 1 -c 1 -o gpurun_out/${TAG}_prof_raster python bench.py --steps 1 --warmup 2 --no-cpu-baseline --no-sweep > gpurun_out/${TAG}_ncu4.txt 2>&1
 tail -3 gpurun_out/${TAG}_pytest.txt; tail -2 gpurun_out/${TAG}_smoke.txt; tail -c 2500 gpurun_out/${TAG}_bench.txt
