@@ -195,22 +195,19 @@ BT_DEV float fast_compact(uint32_t fl, const float4* B, float f0, float f1) {
     return fast_smooth(fl, f0, f1, kp, kp * (1.0f / 6.0f), FastOps::rcp(kp));
 }
 
+// compare chain ordered by frequency (sharp and compact unions dominate
+// blobtree views) instead of an indirect jump table
 BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
-    switch (code) {
-        case 0u: return f_inf();
-        case 1u: return f1;
-        case 2u: return f0;
-        case 3u: return smin(f0, f1);
-        case 4u: return smax(f0, f1);
-        case 5u: return smax(f0, -f1);
-        case 6u:
-        case 7u:
-        case 8u: {
-            const float4 b0 = B[0];
-            return fast_smooth(code - 6u, f0, f1, b0.x, b0.y, b0.z);
-        }
-        default: return fast_compact(code - 9u, B, f0, f1);
+    if (code == 9u) return fast_compact(0u, B, f0, f1);
+    if (code == 3u) return smin(f0, f1);
+    if (code >= 10u) return fast_compact(code - 9u, B, f0, f1);
+    if (code >= 6u) {
+        const float4 b0 = B[0];
+        return fast_smooth(code - 6u, f0, f1, b0.x, b0.y, b0.z);
     }
+    if (code == 4u) return smax(f0, f1);
+    if (code == 5u) return smax(f0, -f1);
+    return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
 }
 
 // Algorithm 3 over the fast blocks (`prm` = this warp's block area), at NP

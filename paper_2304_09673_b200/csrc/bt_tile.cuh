@@ -344,51 +344,45 @@ BT_DEV void march_finish(March& m, bool hit, float t) {
 BT_DEV void march_set_phase(March& m, uint32_t ph) { m.st = (m.st & ~kPhaseMask) | ph; }
 
 // Advance without evaluating until a field value is needed (reference loop
-// head: step computation, saved-sphere reuse, clamp to t1).
+// head, tracer.hpp:115-139: step, saved-sphere reuse, clamp to t1).  The
+// common case is straight-line select code; reusing a saved sample is the
+// rare case and loops.
 BT_DEV void march_advance(March& m, const TraceParams& tp) {
     for (;;) {
         const float r = E::mul(m.f, tp.invL);
+        float tn = E::add(m.t, smax((m.st & kRelax) ? E::mul(tp.relax, r) : r, tp.minStep));
         if (!is_finite(r)) {
             march_finish(m, false, 0.0f);
             return;
         }
-        float step = (m.st & kRelax) ? E::mul(tp.relax, r) : r;
-        step = smax(step, tp.minStep);
-        float tn = E::add(m.t, step);
-        bool reused = false;
-        float fn = 0.0f;
-        if ((m.st & kSaved) && tn >= m.savedT) {
-            if (m.savedT >= E::add(m.t, tp.minStep) && m.savedT <= m.t1) {
-                tn = m.savedT;
-                fn = m.savedF;
-                reused = true;
-            }
+        if ((m.st & kSaved) && tn >= m.savedT) {  // rare: reaching the remembered sphere
+            const bool reuse = m.savedT >= E::add(m.t, tp.minStep) && m.savedT <= m.t1;
             m.st = (m.st & ~kSaved) | kRelax;
-        }
-        if (tn > m.t1) {
-            if (m.t >= m.t1) {
-                march_finish(m, false, 0.0f);
-                return;
+            if (reuse) {
+                // reused sample: never an overshoot, never beyond t1
+                const float fn = m.savedF;
+                tn = m.savedT;
+                if (fn <= tp.hitEps) {
+                    march_finish(m, true, tn);
+                    return;
+                }
+                if (tn >= m.t1) {
+                    march_finish(m, false, 0.0f);
+                    return;
+                }
+                m.t = tn;
+                m.f = fn;
+                continue;
             }
-            tn = m.t1;
-            reused = false;
         }
-        if (!reused) {
-            m.evalT = tn;
-            march_set_phase(m, 2u);
-            return;
-        }
-        // reused sample: never an overshoot
-        if (fn <= tp.hitEps) {
-            march_finish(m, true, tn);
-            return;
-        }
-        if (tn >= m.t1) {
+        const bool beyond = tn > m.t1;
+        if (beyond && m.t >= m.t1) {
             march_finish(m, false, 0.0f);
             return;
         }
-        m.t = tn;
-        m.f = fn;
+        m.evalT = beyond ? m.t1 : tn;
+        march_set_phase(m, 2u);
+        return;
     }
 }
 
@@ -411,50 +405,42 @@ BT_DEV void march_begin(March& m, float t0, float t1, uint32_t slot) {
     march_set_phase(m, 1u);
 }
 
-// One field value consumed (tracer.hpp:115-175).  Every path that continues
-// the march funnels into a single march_advance call site, which keeps the
-// divergent parts of a warp step short.
+// One field value consumed (tracer.hpp:115-175).  In every non-overshoot
+// case the march moves to the sample (evalT, v): hit if v <= eps, miss if a
+// main step reached t1, else advance.  Only the overshoot back-off branches.
 BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     m.evals++;
-    bool advance = false;
-    if (march_phase(m) != 2u) {  // start sample or back-off sample: the march moves to it
-        m.t = m.evalT;
+    const bool step = march_phase(m) == 2u;
+    const float tn = m.evalT;
+    const bool overshoot = step && (m.st & kRelax) &&
+                           (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v)) || v < -tp.hitEps);
+    if (!overshoot) {
+        const bool hit = v <= tp.hitEps;
+        const bool end = step && tn >= m.t1;
+        m.t = tn;
         m.f = v;
-        if (m.f <= tp.hitEps) march_finish(m, true, m.t);
-        else advance = true;
-    } else {
-        const float fn = v, tn = m.evalT;
-        const bool overshoot = (m.st & kRelax) && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(fn)) ||
-                                                   fn < -tp.hitEps);
-        if (!overshoot) {
-            if (fn <= tp.hitEps) march_finish(m, true, tn);
-            else if (tn >= m.t1) march_finish(m, false, 0.0f);
-            else {
-                m.t = tn;
-                m.f = fn;
-                advance = true;
-            }
-        } else {
-            // remember the non-overlapping sphere, back off to the safe one
-            m.savedT = tn;
-            m.savedF = fn;
-            m.st = (m.st & ~kRelax) | kSaved;
-            const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
-            if (tb >= m.savedT) {
-                m.t = m.savedT;
-                m.f = m.savedF;
-                m.st = (m.st & ~kSaved) | kRelax;
-                if (m.f <= tp.hitEps) march_finish(m, true, m.t);
-                else advance = true;
-            } else if (tb > m.t1) {
-                march_finish(m, false, 0.0f);
-            } else {
-                m.evalT = tb;
-                march_set_phase(m, 3u);
-            }
-        }
+        if (hit) march_finish(m, true, tn);
+        else if (end) march_finish(m, false, 0.0f);
+        else march_advance(m, tp);
+        return;
     }
-    if (advance) march_advance(m, tp);
+    // remember the non-overlapping sphere, back off to the safe one
+    m.savedT = tn;
+    m.savedF = v;
+    m.st = (m.st & ~kRelax) | kSaved;
+    const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
+    if (tb >= m.savedT) {
+        m.t = m.savedT;
+        m.f = m.savedF;
+        m.st = (m.st & ~kSaved) | kRelax;
+        if (m.f <= tp.hitEps) march_finish(m, true, m.t);
+        else march_advance(m, tp);
+    } else if (tb > m.t1) {
+        march_finish(m, false, 0.0f);
+    } else {
+        m.evalT = tb;
+        march_set_phase(m, 3u);
+    }
 }
 
 }  // namespace btk
