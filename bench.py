@@ -375,6 +375,27 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
             "path": "bt_params_update (pinned host) -> bt_render_frame -> bt_gbuffer_download (pinned host), wall clock"}
 
 
+def eager_stages(r, cam, cfg, exact, frames: int = 3) -> dict:
+    """Per-stage device ms of eager frames (CUDA events around each stage)."""
+    import ctypes as C
+
+    from paper_2304_09673_b200 import _capi as capi
+    lib, c = r.lib, cfg.to_c()
+    r.profile(True)
+    for _ in range(frames):
+        capi.check(lib.bt_roi(r.ctx, None, 0), "bt_roi")
+        capi.check(lib.bt_voi_build(r.ctx, C.c_float(cfg.hitEpsilon)), "bt_voi_build")
+        capi.check(lib.bt_abuffer_build(r.ctx, C.byref(cam), 0, 0), "bt_abuffer_build")
+        capi.check(lib.bt_trace(r.ctx, C.byref(cam), C.byref(c), 0, 0, int(exact)), "bt_trace")
+        capi.check(lib.bt_normals(r.ctx, C.byref(cam), cfg.normalsMode, int(exact)), "bt_normals")
+    ms, n = r.profile_read()
+    r.profile(False)
+    names = ["roi_voi", "abuffer", "trace", "normals"]
+    out = {names[i]: round(float(ms[i]) / max(int(n[i]), 1), 4) for i in range(4)}
+    out["roi_voi"] = round(out["roi_voi"] * 2, 4)
+    return out
+
+
 def sweep(rd_unused, exact) -> dict:
     """ms/frame vs primitive count on the other configs (device time, 10 frames)."""
     import torch
@@ -400,7 +421,8 @@ def sweep(rd_unused, exact) -> dict:
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 10
         res[name] = {"primitives": len(s.prims), "resolution": f"{s.width}x{s.height}", "ms_per_frame": round(ms, 4),
-                     "Mrays_s": round(s.width * s.height / ms / 1e3, 1)}
+                     "Mrays_s": round(s.width * s.height / ms / 1e3, 1),
+                     "stages_ms": eager_stages(r, s.device_camera, cfg, exact)}
         r.close()
         s.close()
     return res

@@ -28,6 +28,7 @@ struct DevTree {
     const uint32_t* upperProgram = nullptr;// bit31 ? load frontier value : (op<<26 | word)
     uint32_t nFrontier = 0, nUpper = 0;
     uint32_t upperIsChain = 0;  // upper program = F0 (Fi op)*: left comb, register accumulator
+    uint32_t upperIsMinChain = 0;  // ... and every op is a sharp union: exact parallel (value, index) min
 };
 constexpr uint32_t kFrontierMax = 32;
 constexpr size_t kGradSmemBytes = 160 * 1024;  // frontier values kept in shared memory up to this size

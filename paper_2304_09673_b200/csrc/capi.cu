@@ -82,7 +82,7 @@ struct bt_ctx {
     DevBuf<float4> words;
     DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram;
     DevBuf<uint2> frontier;
-    uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0;
+    uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0, upperIsMinChain = 0;
     DevBuf<int32_t> compactAnc;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
@@ -150,6 +150,7 @@ DevTree dev_tree(const bt_ctx* c) {
     t.nFrontier = c->nFrontier;
     t.nUpper = c->nUpper;
     t.upperIsChain = c->upperIsChain;
+    t.upperIsMinChain = c->upperIsMinChain;
     return t;
 }
 
@@ -517,20 +518,46 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
         if (k != nprims) return fail(BT_EINVAL, "primitiveWords do not match the node records");
     }
     // frontier decomposition: subtree sizes in post-order, frontier roots are
-    // the maximal subtrees of <= kFrontierMax nodes
+    // the maximal subtrees of <= cap nodes.  The cap is chosen per tree by a
+    // small cost model of k_gradient: phase 1's critical path (the heaviest
+    // thread's nodes, ~6 units each: parameter loads + 6 evaluations) plus
+    // phase 2's serial length (one unit per upper entry; a left comb of sharp
+    // unions reduces in log steps).
     std::vector<uint32_t> size(nnodes, 1);
     for (uint32_t i = 0; i < nnodes; ++i)
         if (!nodes[i].isPrimitive) size[i] = 1 + size[nodes[i].leftChild] + size[nodes[i].rightChild];
     std::vector<uint2> frontier;
     std::vector<uint32_t> upper;
-    for (uint32_t i = 0; i < nnodes; ++i) {
-        const int32_t p = parentOrd[i];
-        const bool isRoot = size[i] <= kFrontierMax && (p < 0 || size[p] > kFrontierMax);
-        if (isRoot) {
-            upper.push_back(0x80000000u | (uint32_t)frontier.size());
-            frontier.push_back(make_uint2(i + 1 - size[i], i));
-        } else if (size[i] > kFrontierMax) {
-            upper.push_back(program[i]);  // operator (size > 1)
+    bool chain = false, minChain = false;
+    double bestCost = 0.0;
+    for (uint32_t cap : {4u, 8u, 16u, kFrontierMax}) {
+        std::vector<uint2> f;
+        std::vector<uint32_t> u;
+        for (uint32_t i = 0; i < nnodes; ++i) {
+            const int32_t p = parentOrd[i];
+            if (size[i] <= cap && (p < 0 || size[p] > cap)) {
+                u.push_back(0x80000000u | (uint32_t)f.size());
+                f.push_back(make_uint2(i + 1 - size[i], i));
+            } else if (size[i] > cap) {
+                u.push_back(program[i]);  // operator (size > 1)
+            }
+        }
+        // left comb: LOAD, then (LOAD, OP) pairs -- every operator folds the
+        // running value with a fresh load
+        bool ch = !u.empty() && (u[0] >> 31) && (u.size() % 2 == 1);
+        for (size_t j = 1; ch && j < u.size(); j += 2) ch = (u[j] >> 31) && !(u[j + 1] >> 31);
+        bool mc = ch;
+        for (size_t j = 2; mc && j < u.size(); j += 2) mc = ((u[j] >> 26) & 0x1Fu) == 3u;
+        std::vector<uint32_t> load(256, 0);
+        for (size_t j = 0; j < f.size(); ++j) load[j % 256] += f[j].y - f[j].x + 1;
+        const double phase1 = 6.0 * *std::max_element(load.begin(), load.end());
+        const double phase2 = mc ? 10.0 + (double)(u.size() / 2 + 31) / 32 : (double)u.size();
+        if (frontier.empty() || phase1 + phase2 < bestCost) {
+            bestCost = phase1 + phase2;
+            frontier.swap(f);
+            upper.swap(u);
+            chain = ch;
+            minChain = mc;
         }
     }
     // full post-order stack depth
@@ -567,11 +594,8 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->upperProgram.ptr, upper.data(), upper.size() * 4, cudaMemcpyHostToDevice, c->stream));
     c->nFrontier = (uint32_t)frontier.size();
     c->nUpper = (uint32_t)upper.size();
-    {  // left comb: LOAD, then (LOAD, OP) pairs -- every operator folds the running value with a fresh load
-        bool chain = !upper.empty() && (upper[0] >> 31) && (upper.size() % 2 == 1);
-        for (size_t j = 1; chain && j < upper.size(); j += 2) chain = (upper[j] >> 31) && !(upper[j + 1] >> 31);
-        c->upperIsChain = chain ? 1u : 0u;
-    }
+    c->upperIsChain = chain ? 1u : 0u;
+    c->upperIsMinChain = minChain ? 1u : 0u;
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->nwords = nwords;
     c->nnodes = nnodes;

@@ -327,7 +327,9 @@ __global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* cou
 // p +- h e_axis, h = max(1e-3, 1e-4 t).  One CTA per queued pixel:
 //   phase 1  every (frontier subtree, tap) pair is evaluated by one thread
 //            (post-order over <= 32 nodes) -- independent work;
-//   phase 2  six threads run the upper operator program over those values.
+//   phase 2  six threads run the upper operator program over those values;
+//            a left comb of sharp unions is a (value, index) min-reduction
+//            (one warp per tap), exact because std::min keeps the earliest.
 // Each node still combines exactly the same operands in the same order as
 // the reference's serial walk, so the exact variant stays bit-identical.
 // One frontier subtree at the 6 gradient taps: parameters are loaded once per
@@ -396,7 +398,39 @@ __global__ void __launch_bounds__(256) k_gradient(DevTree t, Cam cam, FrameBufs 
             for (int k = 0; k < 6; ++k) vals[f * 6u + k] = v6[k];
         }
         __syncthreads();
-        if (threadIdx.x < 6 && t.upperIsChain) {
+        if (t.upperIsMinChain) {
+            // min over the chain's values in order (csg union == std::min, the
+            // earliest minimum wins): exact as a (value, index) reduction --
+            // warp w reduces tap w.
+            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            if (w < 6) {
+                const uint32_t m = (t.nUpper + 1) / 2;  // values in the chain
+                float best = f_inf();
+                uint32_t bestIdx = 0xFFFFFFFFu;
+                for (uint32_t q = lane; q < m; q += 32) {
+                    const float v = vals[(upper[q == 0 ? 0 : 2 * q - 1] & 0x7FFFFFFFu) * 6u + w];
+                    if (!(v != v) && (bestIdx == 0xFFFFFFFFu || v < best)) {  // NaN never wins b < a
+                        best = v;
+                        bestIdx = q;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(kFull, best, o);
+                    const uint32_t oi = __shfl_xor_sync(kFull, bestIdx, o);
+                    const bool take = oi != 0xFFFFFFFFu &&
+                                      (bestIdx == 0xFFFFFFFFu || ov < best || (!(best < ov) && oi < bestIdx));
+                    if (take) {
+                        best = ov;
+                        bestIdx = oi;
+                    }
+                }
+                if (lane == 0) {  // ... unless it is the accumulator's first value
+                    const float v0 = vals[(upper[0] & 0x7FFFFFFFu) * 6u + w];
+                    res[w] = (v0 != v0) ? v0 : best;
+                }
+            }
+        } else if (threadIdx.x < 6 && t.upperIsChain) {
             // left comb: acc = F0; acc = op(acc, Fi) -- same operand order as the
             // post-order walk, no stack traffic on the serial dependency chain
             float acc = vals[(upper[0] & 0x7FFFFFFFu) * 6u + threadIdx.x];

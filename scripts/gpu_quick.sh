@@ -8,5 +8,5 @@ python - "$TAG" <<'PY'
 import json,sys
 for l in open(f"gpurun_out/{sys.argv[1]}_bench.txt"):
     if l.startswith("{"):
-        d=json.loads(l); print("frame_ms", d["ms_per_step"], "Mrays/s", d["value"], "stages", d["stages_ms"], "frac", d["roofline"]["frac"], "e2e", d.get("e2e",{}).get("value"), "sweep", {k:v["ms_per_frame"] for k,v in d.get("sweep_ms_per_frame",{}).items()})
+        d=json.loads(l); print("frame_ms", d["ms_per_step"], "Mrays/s", d["value"], "stages", d["stages_ms"], "frac", d["roofline"]["frac"], "e2e", d.get("e2e",{}).get("value"), "sweep", {k:(v["ms_per_frame"], v.get("stages_ms")) for k,v in d.get("sweep_ms_per_frame",{}).items()})
 PY
