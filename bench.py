@@ -14,7 +14,7 @@ synchronized sphere tracing -> normals, replayed from one CUDA graph.
 * e2e         the same through the public C-ABI with HOST buffers: pinned
               H2D of the frame's parameter deltas and D2H of the whole
               G-buffer (hit, depth, normal, evalCount, tile planes) per step.
-* roofline    the field-evaluation kernel (k_trace) against the measured FP32
+* roofline    the field-evaluation kernel (k_march) against the measured FP32
               (FFMA) peak of the box: algorithmic flops per frame (SURVEY.md
               appendix B, counted on the device) / the kernel's CUDA-event time.
 * cpu_baseline the unmodified reference (oracle/_ref) timed on this host's
@@ -272,11 +272,12 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     stage_ms, flops_per_frame, st = stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim)
     peak = C.c_float()
     capi.check(lib.bt_fp32_peak(local_rank, C.byref(peak), None), "bt_fp32_peak")
-    trace_ms = stage_ms["trace"]
-    achieved = flops_per_frame / (trace_ms * 1e-3) / 1e12
+    march_ms = stage_ms["trace_march"]
+    achieved = flops_per_frame / (march_ms * 1e-3) / 1e12
     result["stages_ms"] = {k: round(v, 4) for k, v in stage_ms.items()}
     result["roofline"] = {
-        "kernel": "k_trace (synchronized per-tile sphere tracing + field evaluation)",
+        "kernel": "k_march (synchronized per-tile sphere tracing + field evaluation)",
+        "kernel_ms": round(march_ms, 4),
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak.value, 2), "unit": "TFLOP/s",
         "frac": round(achieved / peak.value, 4), "traffic": None,
         "peak_source": "measured FFMA microbenchmark on this box (bt_fp32_peak); MEASURED_PEAKS.json has no FP32 figure",
@@ -330,10 +331,10 @@ def stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim, fra
         capi.check(lib.bt_normals(rd.ctx, C.byref(cam), cfg.normalsMode, int(exact)), "bt_normals")
         st = rd.stats()
         flops.append(st.fieldFlops)
-    ms, n = rd.profile_read()
+    ms, n = rd.profile_read_ex()
     rd.profile(False)
-    names = ["roi_voi", "abuffer", "trace", "normals"]
-    stage = {names[i]: float(ms[i]) / max(int(n[i]), 1) for i in range(4)}
+    names = ["roi_voi", "abuffer", "trace", "normals", "trace_views", "trace_march"]
+    stage = {names[i]: float(ms[i]) / max(int(n[i]), 1) for i in range(6)}
     stage["roi_voi"] *= 2  # roi and voi are two profiled calls per frame
     return stage, float(np.mean(flops)), st
 
@@ -388,10 +389,10 @@ def eager_stages(r, cam, cfg, exact, frames: int = 3) -> dict:
         capi.check(lib.bt_abuffer_build(r.ctx, C.byref(cam), 0, 0), "bt_abuffer_build")
         capi.check(lib.bt_trace(r.ctx, C.byref(cam), C.byref(c), 0, 0, int(exact)), "bt_trace")
         capi.check(lib.bt_normals(r.ctx, C.byref(cam), cfg.normalsMode, int(exact)), "bt_normals")
-    ms, n = r.profile_read()
+    ms, n = r.profile_read_ex()
     r.profile(False)
-    names = ["roi_voi", "abuffer", "trace", "normals"]
-    out = {names[i]: round(float(ms[i]) / max(int(n[i]), 1), 4) for i in range(4)}
+    names = ["roi_voi", "abuffer", "trace", "normals", "trace_views", "trace_march"]
+    out = {names[i]: round(float(ms[i]) / max(int(n[i]), 1), 4) for i in range(6)}
     out["roi_voi"] = round(out["roi_voi"] * 2, 4)
     return out
 

@@ -218,6 +218,10 @@ BT_API int bt_stats_reset(bt_ctx* ctx);
  * reset when profiling is enabled: [roi_voi, abuffer, trace, normals]. */
 BT_API int bt_profile_enable(bt_ctx* ctx, int on);
 BT_API int bt_profile_read(bt_ctx* ctx, float* ms4, uint32_t* launches4);
+/* Up to 6 slots: the 4 above, then the two halves of trace: [4] interval /
+ * view compilation (k_view_count, k_view_scan, k_view_build), [5] the march
+ * kernel alone (k_march: field evaluation -- the roofline kernel). */
+BT_API int bt_profile_read_ex(bt_ctx* ctx, float* ms, uint32_t* launches, uint32_t nslots);
 /* Measured non-tensor FP32 peak of `device` (FFMA microbenchmark, TFLOP/s):
  * the roofline denominator of the field-evaluation kernel. */
 BT_API int bt_fp32_peak(int device, float* tflops, float* ms);

@@ -98,6 +98,7 @@ PROTOTYPES = {
     "bt_stats_reset": [vp],
     "bt_profile_enable": [vp, C.c_int],
     "bt_profile_read": [vp, vp, vp],
+    "bt_profile_read_ex": [vp, vp, vp, C.c_uint32],
     "bt_fp32_peak": [C.c_int, P(f32), P(f32)],
     "bt_graph_kernel_count": [vp, P(u32), P(u32)],
 }

@@ -5,7 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "bt_tile.cuh"
+#include "bt_views.cuh"
 
 namespace btk {
 
@@ -124,10 +124,17 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
                     int smCount);
 void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
 
+// ---- launchers (k_views.cu) -------------------------------------------
+// build=false: count pass + scan (the host may then read the totals and grow
+// the record buffers); build=true: write the interval/view records.
+void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
+                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build);
+uint32_t view_scan_blocks(uint32_t tiles);
+
 // ---- launchers (k_trace.cu) -------------------------------------------
-void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
-                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
-                  uint32_t tile0, uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue);
+void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
+                  const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
+                  uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue);
 size_t trace_scratch_float4s(int smCount);
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,

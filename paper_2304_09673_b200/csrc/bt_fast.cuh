@@ -89,9 +89,11 @@ BT_DEV float f_sphere(float4 c, F3 p) {
     const float dx = p.x - c.x, dy = p.y - c.y, dz = p.z - c.z;
     return fsqrt(dx * dx + dy * dy + dz * dz) - c.w;
 }
+// three FFMAs per row: the translation is the chain's seed
 BT_DEV F3 f_affine(float4 r0, float4 r1, float4 r2, F3 p) {
-    return F3{r0.x * p.x + r0.y * p.y + r0.z * p.z + r0.w, r1.x * p.x + r1.y * p.y + r1.z * p.z + r1.w,
-              r2.x * p.x + r2.y * p.y + r2.z * p.z + r2.w};
+    return F3{fmaf(r0.x, p.x, fmaf(r0.y, p.y, fmaf(r0.z, p.z, r0.w))),
+              fmaf(r1.x, p.x, fmaf(r1.y, p.y, fmaf(r1.z, p.z, r1.w))),
+              fmaf(r2.x, p.x, fmaf(r2.y, p.y, fmaf(r2.z, p.z, r2.w)))};
 }
 BT_DEV float f_box(float4 e, F3 l) {
     const float qx = fabsf(l.x) - e.x, qy = fabsf(l.y) - e.y, qz = fabsf(l.z) - e.z;
@@ -210,15 +212,14 @@ BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
     return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
 }
 
-// Algorithm 3 over the fast blocks (`prm` = this warp's block area), at NP
-// points per lane (NP = 2 when both of a lane's ray slots are marching).
+// Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks,
+// normally in this warp's shared memory), at NP points per lane.
 template <int NP>
-BT_DEV void eval_view_fast(const WarpSmem& s, const float4* prm, const F3* p, float* out) {
+BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, const F3* p, float* out) {
     float stk[NP][kStackCap];
     uint32_t sp = 0;
-    const uint32_t n = s.nView;
     for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t b = s.vHdr[i];
+        const uint32_t b = hdr[i];
         const float4* B = prm + (b & 0xFFFFu);
         if (blob_is_prim(b)) {
             float v[NP];

@@ -71,6 +71,8 @@ struct FrameKey {
 
 }  // namespace
 
+constexpr int kProfSlots = 6;
+
 struct bt_ctx {
     int device = 0;
     int smCount = 148;
@@ -113,7 +115,11 @@ struct bt_ctx {
     bool haveGbuffer = false;
 
     DevBuf<uint64_t> stats;
-    DevBuf<float4> traceScratch;  // per-warp fast parameter blocks of k_trace
+    // compiled intervals / pruned views of stage (c) (k_views.cu)
+    DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
+    DevBuf<IntervalRec> vIv;
+    DevBuf<uint32_t> vCounters;
+    DevBuf<float4> traceScratch;  // per-warp fast parameter blocks of k_march (views too large for smem)
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
@@ -126,9 +132,11 @@ struct bt_ctx {
 
     // profiling (CUDA events around each stage)
     bool profiling = false;
-    float profMs[4] = {0, 0, 0, 0};
-    uint32_t profLaunch[4] = {0, 0, 0, 0};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    // slots: 0 roi+voi, 1 abuffer, 2 trace (all of stage c), 3 normals,
+    //        4 k_view_* (interval/view compilation), 5 k_march (field evaluation)
+    float profMs[kProfSlots] = {};
+    uint32_t profLaunch[kProfSlots] = {};
+    cudaEvent_t ev[6] = {};
 };
 
 namespace {
@@ -176,6 +184,20 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.pairCap = c->pairs.cap;
     f.poolCap = c->pool.cap;
     return f;
+}
+
+ViewBufs view_bufs(const bt_ctx* c) {
+    ViewBufs v;
+    v.count = c->vCount.ptr;
+    v.local = c->vLocal.ptr;
+    v.blockSum = c->vBlockSum.ptr;
+    v.blockPrefix = c->vBlockPrefix.ptr;
+    v.iv = c->vIv.ptr;
+    v.nodes = c->vNodes.ptr;
+    v.counters = c->vCounters.ptr;
+    v.ivCap = c->vIv.cap;
+    v.nodeCap = c->vNodes.cap;
+    return v;
 }
 
 GBuf gbuf(const bt_ctx* c) {
@@ -238,6 +260,12 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->tileMaxOverlap.reserve(tiles));
     BT_CUDA(c->tileCacheBytes.reserve(tiles));
     BT_CUDA(c->tileError.reserve(tiles));
+    const size_t nvscan = view_scan_blocks((uint32_t)tiles);
+    BT_CUDA(c->vCount.reserve(tiles));
+    BT_CUDA(c->vLocal.reserve(tiles));
+    BT_CUDA(c->vBlockSum.reserve(nvscan));
+    BT_CUDA(c->vBlockPrefix.reserve(nvscan + 1));
+    BT_CUDA(c->vCounters.reserve(2));
     c->haveAbuffer = false;
     c->haveRays = false;
     c->haveGbuffer = false;
@@ -346,15 +374,58 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
     return BT_OK;
 }
 
+// Stage (c): compile the tiles' intervals and views (count, scan, build), then
+// march.  In `checked` mode the record totals are read back after the scan
+// and the record buffers grown (2x headroom) before the build; inside a graph
+// replay an overflow is flagged (bt_stats_download) and the tiles marked.
 int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
-             int exact) {
+             int exact, bool checked) {
     if (c->traceScratch.cap == 0) {
         BT_CUDA(c->traceScratch.reserve(trace_scratch_float4s(c->smCount)));
         BT_CUDA(c->tileQueue.reserve(1));
         c->bufEpoch++;
     }
-    launch_trace(c->stream, exact != 0, dev_tree(c), to_cam(cam), trace_params(cfg, cam), frame_bufs(c), gbuf(c),
-                 c->stats.ptr, tile0, tile1, c->smCount, c->traceScratch.ptr, c->tileQueue.ptr);
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    if (c->vIv.cap == 0) {
+        BT_CUDA(c->vIv.reserve(std::max<size_t>(1u << 16, (size_t)tiles * 2)));
+        BT_CUDA(c->vNodes.reserve(std::max<size_t>(1u << 18, (size_t)tiles * 8)));
+        c->bufEpoch++;
+    }
+    const DevTree t = dev_tree(c);
+    const Cam k = to_cam(cam);
+    const TraceParams tp = trace_params(cfg, cam);
+    if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
+    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+    if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
+    if (checked) {
+        uint2 total{0u, 0u};
+        BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
+                                cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        if (total.x > c->vIv.cap || total.y > c->vNodes.cap) {
+            if (total.x > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)total.x * 2));
+            if (total.y > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)total.y * 2));
+            c->bufEpoch++;
+            launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+        }
+    }
+    if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
+    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
+    if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
+    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), view_bufs(c), gbuf(c), c->stats.ptr, tile0, tile1,
+                 c->smCount, c->traceScratch.ptr, c->tileQueue.ptr);
+    if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
+        cudaEventRecord(c->ev[1], c->stream);
+        cudaEventSynchronize(c->ev[1]);
+        float a = 0.f, b = 0.f, m = 0.f;
+        cudaEventElapsedTime(&a, c->ev[2], c->ev[3]);
+        cudaEventElapsedTime(&b, c->ev[4], c->ev[5]);
+        cudaEventElapsedTime(&m, c->ev[5], c->ev[1]);
+        c->profMs[4] += a + b;
+        c->profMs[5] += m;
+        c->profLaunch[4] += 1;
+        c->profLaunch[5] += 1;
+    }
     c->haveGbuffer = true;
     return BT_OK;
 }
@@ -407,8 +478,7 @@ int bt_ctx_create(int device, bt_ctx** out) {
         return fail(BT_ECUDA, cudaGetErrorString(e));
     }
     c->stream = c->own;
-    cudaEventCreate(&c->ev[0]);
-    cudaEventCreate(&c->ev[1]);
+    for (auto& e : c->ev) cudaEventCreate(&e);
     if (c->stats.reserve(kStSlots) != cudaSuccess || c->counters.reserve(kCntSlots) != cudaSuccess) {
         delete c;
         return fail(BT_ENOMEM, "cannot allocate statistics");
@@ -451,9 +521,11 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->stats.release();
     c->gradScratch.release();
     c->traceScratch.release();
+    for (auto* b : {&c->vCount, &c->vLocal, &c->vBlockSum, &c->vBlockPrefix, &c->vNodes}) b->release();
+    c->vIv.release();
+    c->vCounters.release();
     c->tileQueue.release();
-    cudaEventDestroy(c->ev[0]);
-    cudaEventDestroy(c->ev[1]);
+    for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->own);
     delete c;
     return BT_OK;
@@ -815,7 +887,7 @@ int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint3
     rc = resolve_tiles(c, tile0, tile1);
     if (rc) return rc;
     prof_begin(c);
-    rc = do_trace(c, *cam, *cfg, tile0, tile1, exact);
+    rc = do_trace(c, *cam, *cfg, tile0, tile1, exact, true);
     prof_end(c, 2);
     return rc;
 }
@@ -873,7 +945,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         if (r) return r;
         r = do_abuffer(c, *cam, tile0, tile1, checked);
         if (r) return r;
-        r = do_trace(c, *cam, *cfg, tile0, tile1, exact);
+        r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked);
         if (r) return r;
         return normals ? do_normals(c, *cam, mode, exact) : BT_OK;
     };
@@ -1012,6 +1084,12 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
     }
     if (cnt[kCntOverflow] || cnt[kCntPairs] > c->pairs.cap)
         return fail(BT_ENOMEM, "A-buffer capacity overflowed during a graph replay; re-run eagerly");
+    if (c->vCounters.ptr) {
+        uint32_t vc[2] = {0u, 0u};
+        BT_CUDA(cudaMemcpyAsync(vc, c->vCounters.ptr, sizeof(vc), cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        if (vc[1]) return fail(BT_ENOMEM, "interval-record capacity overflowed during a graph replay; re-run eagerly");
+    }
     return BT_OK;
 }
 
@@ -1024,18 +1102,20 @@ int bt_stats_reset(bt_ctx* c) {
 int bt_profile_enable(bt_ctx* c, int on) {
     if (!c) return fail(BT_EINVAL, "ctx is null");
     c->profiling = on != 0;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kProfSlots; ++i) {
         c->profMs[i] = 0.f;
         c->profLaunch[i] = 0;
     }
     return BT_OK;
 }
 
-int bt_profile_read(bt_ctx* c, float* ms4, uint32_t* l4) {
+int bt_profile_read(bt_ctx* c, float* ms4, uint32_t* l4) { return bt_profile_read_ex(c, ms4, l4, 4); }
+
+int bt_profile_read_ex(bt_ctx* c, float* ms, uint32_t* launches, uint32_t nslots) {
     if (!c) return fail(BT_EINVAL, "ctx is null");
-    for (int i = 0; i < 4; ++i) {
-        if (ms4) ms4[i] = c->profMs[i];
-        if (l4) l4[i] = c->profLaunch[i];
+    for (uint32_t i = 0; i < nslots && i < (uint32_t)kProfSlots; ++i) {
+        if (ms) ms[i] = c->profMs[i];
+        if (launches) launches[i] = c->profLaunch[i];
     }
     return BT_OK;
 }

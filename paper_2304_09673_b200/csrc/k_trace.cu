@@ -1,15 +1,19 @@
-// k_trace.cu -- stage (c) on sm_100a: synchronized per-tile sphere tracing,
-// normals, and the GPU brute-force oracle.
+// k_trace.cu -- stage (c) on sm_100a, part 2: synchronized sphere tracing
+// over the compiled intervals (k_views.cu), normals, and the GPU brute-force
+// oracle.
 //
-//   k_trace<O>     one warp per 8x8 tile, two pixel rays per lane; lane 0
-//                  runs fetch_interval + view build (tracer.cpp:50-103,
-//                  traversal.cpp:88-99) in shared memory, then all 64 rays
-//                  march in lockstep over the pruned view with warp votes
-//                  retiring finished rays (render_tiles, tracer.cpp:141-236).
+//   k_march<O>     one warp per 8x8 tile (persistent, tile queue).  Per
+//                  interval record: stage the pruned view into this warp's
+//                  shared memory (fast path: lane-parallel conversion into
+//                  evaluation-ready parameter blocks), then march the tile's
+//                  unfinished rays in lockstep.  Rays are served from a
+//                  warp-synchronous queue: a lane whose ray finished takes the
+//                  next pending ray of the interval (ballot + popc rank), so
+//                  64 rays keep 32 lanes busy until the queue drains
+//                  (render_tiles, tracer.cpp:141-236).
 //   k_normals      depth-differential normals (tracer.cpp:296-350); pixels
 //                  without usable neighbours are queued for k_gradient.
-//   k_gradient<O>  one warp per queued pixel, lanes 0..5 each run one full
-//                  post-order tree walk (eval_full, traversal.cpp:126-141).
+//   k_gradient<O>  6-tap eval_full fallback (traversal.cpp:126-141).
 //   k_oracle<O>    oracle_render (tracer.cpp:238-280): every pixel marched
 //                  over [near, far] on the full tree.
 //
@@ -20,6 +24,7 @@
 
 #include "bt_device.h"
 #include "bt_fast.cuh"
+#include "bt_views.cuh"
 
 namespace btk {
 
@@ -28,26 +33,23 @@ namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kTraceWarps = 4;
 constexpr int kFullStackCap = 128;
+constexpr uint32_t kMarchBlocks = 320;  // float4s of fast parameter blocks kept in shared memory per warp
+constexpr uint32_t kNoRay = 0xFFFFFFFFu;
 
 template <class O> __device__ __forceinline__ F3 ray_point(F3 o, F3 d, float t) {
     return vadd<O>(o, vscale<O>(d, t));
-}
-
-struct RayLane {
-    March m;
-    F3 dir;
-};
-
-__device__ __forceinline__ void swap_lanes(RayLane& a, RayLane& b) {
-    const RayLane t = a;
-    a = b;
-    b = t;
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
 template <class O> struct IsFast {
@@ -57,180 +59,210 @@ template <> struct IsFast<FastOps> {
     static constexpr bool value = true;
 };
 
-// One 8x8 tile, executed by one warp (see the file comment).
-template <class O>
-__device__ __forceinline__ void trace_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
-                                           const FrameBufs& fb, const GBuf& g, uint64_t* stats, WarpSmem& s,
-                                           float4* prm, int lane, uint32_t tile) {
-    const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
+// Per-warp shared memory of k_march.
+struct MarchSmem {
+    float4 blocks[kMarchBlocks];  // fast parameter blocks of the staged view
+    float4 rays[64];              // dir.xyz, dot(dir, forward) of the tile's rays
+    uint32_t hdr[kViewCap];       // staged view: isPrim(1) op(5) | block offset
+    uint32_t word[kViewCap];      // exact path: tree word of each node's parameters
+    float depth[64];
+    uint32_t evals[64];
+    uint8_t hit[64];
+    uint8_t pend[64];             // rays still to march in this interval, in order
+};
 
+// Per-block work accounting, flushed to the device statistics once per CTA.
+struct BlockStats {
+    unsigned long long fe, rnv, pe, fl, steps, errs;
+    unsigned int maxOv, maxCache;
+};
+
+// March the pending rays of one interval over the staged view.
+template <class O>
+__device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam, const TraceParams& tp, MarchSmem& s,
+                                               const float4* blk, uint32_t nView, uint32_t nPend, float vz0, float vz1,
+                                               uint32_t lt, uint32_t& fe, uint32_t& fl, uint32_t& steps,
+                                               uint32_t flops) {
+    uint32_t cursor = 0, ray = kNoRay;
+    March m;
+    march_idle(m, 0u);
+    m.evalT = 0.0f;
+    F3 dir{0.f, 0.f, 1.f};
+    for (;;) {
+        const bool idle = march_phase(m) == 0u;
+        if (idle && ray != kNoRay) {  // record the ray that just finished
+            const uint32_t e = m.evals;
+            s.evals[ray] += e;
+            if (march_hit(m)) {
+                s.hit[ray] = 1;
+                s.depth[ray] = m.t;
+            }
+            fe += e;
+            fl += e * flops;
+            ray = kNoRay;
+        }
+        const uint32_t idleMask = __ballot_sync(kFull, idle);
+        if (idleMask != 0u && cursor < nPend) {  // refill idle lanes from the queue
+            const uint32_t rank = cursor + __popc(idleMask & lt);
+            if (idle && rank < nPend) {
+                ray = s.pend[rank];
+                const float4 r = s.rays[ray];
+                dir = F3{r.x, r.y, r.z};
+                march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w), 0u);
+            }
+            cursor += __popc(idleMask);
+        }
+        if (!__any_sync(kFull, march_phase(m) != 0u)) {
+            if (cursor >= nPend) break;
+            continue;
+        }
+        ++steps;
+        const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
+        float v;
+        if (IsFast<O>::value) eval_view_fast<1>(s.hdr, nView, blk, &p, &v);
+        else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);
+        if (march_phase(m) != 0u) march_consume(m, v, tp);
+    }
+}
+
+// One 8x8 tile: walk its compiled intervals until all 64 rays have hit
+// (tracer.cpp:165-230), then write its pixels and tile planes.
+template <class O>
+__device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
+                                           const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
+                                           float4* gblk, BlockStats& bs, int lane, uint32_t tile) {
+    const uint32_t lt = lanemask_lt();
+    const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
     int px[2], py[2];
-    bool valid[2], found[2], hitf[2] = {false, false};
-    float depth[2] = {0.0f, 0.0f};
-    uint32_t evals[2] = {0u, 0u};
+    bool valid[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int li = lane + 32 * j;
         px[j] = tx * kTile + (li & 7);
         py[j] = ty * kTile + (li >> 3);
         valid[j] = px[j] < g.width && py[j] < g.height;
-        found[j] = !valid[j];
+        s.hit[li] = 0;
+        s.evals[li] = 0;
     }
-    const uint32_t off = fb.offsets[tile];
-    const uint32_t cnt = fb.offsets[tile + 1] - off;
-    const Frag* list = fb.frags + off;
-
+    uint32_t found0 = ~__ballot_sync(kFull, valid[0]), found1 = ~__ballot_sync(kFull, valid[1]);
     uint32_t tileMaxOv = 0, tileCache = 0, tileErr = 0;
-    uint64_t stFE = 0, stRNV = 0, stPE = 0, stFL = 0;
-    uint32_t warpSteps = 0;
-
-    if (cnt != 0) {
-        F3 dir[2];
-        float ddf[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            dir[j] = F3{0.f, 0.f, 1.f};
-            ddf[j] = 1.0f;
-            if (valid[j]) {
-                const float4 r = fb.rays[(size_t)tile * 64 + lane + 32 * j];
-                dir[j] = F3{r.x, r.y, r.z};
-                ddf[j] = r.w;
-            }
-        }
-        for (uint32_t i = lane; i < cnt && i < (uint32_t)kFragStage; i += 32) s.stage[i] = list[i];
-        if (lane == 0) {
-            s.nAct = 0;
-            s.cursor = 0;
-            s.zEnd = 0.0f;
-            s.err = 0;
-        }
-        __syncwarp();
-
-        for (;;) {
-            if (__all_sync(kFull, found[0] && found[1])) break;
-            if (lane == 0) {
-                uint32_t fetched = 0;
-                const bool ok = fetch_interval(s, list, cnt, cam, tp, fetched);
-                s.done = ok ? 0u : 1u;
-                if (ok) build_view(s, t.words);
-            }
-            __syncwarp();
-            if (s.done) break;
-            const uint32_t overlap = s.nAct;
-            tileMaxOv = max(tileMaxOv, overlap);
-            if (s.err) {
+    uint32_t fe = 0, rnv = 0, pe = 0, fl = 0, steps = 0;
+    const uint2 c = vb.count[tile];
+    if (c.x != 0u && vb.counters[1] != 0u) {
+        tileErr = 1;  // interval records overflowed in a graph replay (flagged to the host)
+    } else if (c.x != 0u) {
+        const uint2 o = view_offset(vb, tile);
+        s.rays[lane] = fb.rays[(size_t)tile * 64 + lane];
+        s.rays[lane + 32] = fb.rays[(size_t)tile * 64 + lane + 32];
+        for (uint32_t k = 0; k < c.x; ++k) {
+            if ((found0 & found1) == kFull) break;
+            const uint4* rp = reinterpret_cast<const uint4*>(vb.iv + o.x + k);
+            const uint4 ra = rp[0], rb = rp[1];
+            const uint32_t flags = rb.x >> 8;
+            tileMaxOv = max(tileMaxOv, rb.x & 0xFFu);
+            if (flags & kIvErr) {
                 tileErr = 1;
                 break;
             }
-            tileCache = max(tileCache, s.cacheFloats * 4u);
-            if (!s.rootUsed) continue;
-            const float zb = s.zBegin, ze = s.zEnd;
+            tileCache = max(tileCache, rb.y);
+            if (!(flags & kIvRootUsed)) continue;
+            const float zb = __uint_as_float(ra.x), ze = __uint_as_float(ra.y);
             if (ze <= zb) continue;
-            if (s.maxDepth > kStackCap) {  // eval_pruned would throw on first use
+            if (flags & kIvDepthErr) {  // eval_pruned would throw on first use
                 tileErr = 1;
                 break;
             }
-            if (IsFast<O>::value) {  // lane-parallel parameter-block conversion
-                for (uint32_t i = lane; i < s.nView; i += 32)
-                    convert_node(s.vBlob[i], t.words + s.vWord[i] + 1, prm + (s.vHdr[i] & 0xFFFFu));
-                __syncwarp();
+            const uint32_t nView = ra.w & 0xFFFFu, nPrim = ra.w >> 16;
+            float4* blk = rb.w <= kMarchBlocks ? s.blocks : gblk;
+            for (uint32_t i = lane; i < nView; i += 32) {
+                const uint2 nd = vb.nodes[ra.z + i];
+                s.hdr[i] = nd.x;
+                if (IsFast<O>::value) convert_node(nd.x, t.words + nd.y + 1, blk + (nd.x & 0xFFFFu));
+                else s.word[i] = nd.y;
             }
-            const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
-            // Two ray slots per lane, served one after the other: `cur` is the
-            // slot being marched, `oth` the other one.  Each step evaluates the
-            // field once per lane (one instantiation of the evaluator keeps the
-            // hot loop inside the instruction cache).
-            RayLane cur, oth;
-            cur.dir = dir[0];
-            oth.dir = dir[1];
-            if (!found[0]) march_begin(cur.m, E::div(vz0, ddf[0]), E::div(vz1, ddf[0]), 0u);
-            else march_idle(cur.m, 0u);
-            if (!found[1]) march_begin(oth.m, E::div(vz0, ddf[1]), E::div(vz1, ddf[1]), 1u);
-            else march_idle(oth.m, 1u);
-            if (march_phase(cur.m) == 0u && march_phase(oth.m) != 0u) swap_lanes(cur, oth);
-            while (__any_sync(kFull, march_phase(cur.m) != 0u)) {
-                ++warpSteps;
-                const F3 p = ray_point<O>(cam.pos, cur.dir, cur.m.evalT);
-                float v;
-                if (IsFast<O>::value) eval_view_fast<1>(s, prm, &p, &v);
-                else v = eval_view<O>(s, t.words, p);
-                if (march_phase(cur.m) != 0u) {
-                    march_consume(cur.m, v, tp);
-                    if (march_phase(cur.m) == 0u && march_phase(oth.m) != 0u) swap_lanes(cur, oth);
-                }
-            }
-            const uint32_t nView = s.nView, nPrim = s.nPrim, fl = s.flops;
-            const bool curIs0 = (cur.m.st & kSlot1) == 0u;
-            const March& m0 = curIs0 ? cur.m : oth.m;
-            const March& m1 = curIs0 ? oth.m : cur.m;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const March& mj = j == 0 ? m0 : m1;
-                if (found[j]) continue;
-                const uint32_t e = mj.evals;
-                evals[j] += e;
-                stFE += e;
-                stRNV += (uint64_t)e * nView;
-                stPE += (uint64_t)e * nPrim;
-                stFL += (uint64_t)e * fl;
-                if (march_hit(mj)) {
-                    found[j] = true;
-                    hitf[j] = true;
-                    depth[j] = mj.t;
-                }
-            }
+            // queue of this interval: the tile's unfinished rays, in ray order
+            const uint32_t p0 = ~found0, p1 = ~found1;
+            const uint32_t c0 = __popc(p0), nPend = c0 + __popc(p1);
+            if ((p0 >> lane) & 1u) s.pend[__popc(p0 & lt)] = (uint8_t)lane;
+            if ((p1 >> lane) & 1u) s.pend[c0 + __popc(p1 & lt)] = (uint8_t)(lane + 32);
             __syncwarp();
+            const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
+            uint32_t ife = 0, ifl = 0;
+            march_interval<O>(t, cam, tp, s, blk, nView, nPend, vz0, vz1, lt, ife, ifl, steps, rb.z);
+            fe += ife;
+            fl += ifl;
+            rnv += ife * nView;
+            pe += ife * nPrim;
+            __syncwarp();
+            found0 |= __ballot_sync(kFull, s.hit[lane] != 0);
+            found1 |= __ballot_sync(kFull, s.hit[lane + 32] != 0);
         }
     }
-
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         if (!valid[j]) continue;
+        const int li = lane + 32 * j;
         const size_t p = (size_t)py[j] * g.width + px[j];
-        g.hit[p] = hitf[j] ? 1 : 0;
-        g.depth[p] = hitf[j] ? depth[j] : 0.0f;
-        g.evalCount[p] = evals[j];
+        const bool h = s.hit[li] != 0;
+        g.hit[p] = h ? 1 : 0;
+        g.depth[p] = h ? s.depth[li] : 0.0f;
+        g.evalCount[p] = s.evals[li];
     }
-    stFE = warp_sum_u64(stFE);
-    stRNV = warp_sum_u64(stRNV);
-    stPE = warp_sum_u64(stPE);
-    stFL = warp_sum_u64(stFL);
+    const uint64_t sfe = warp_sum_u64(fe), srnv = warp_sum_u64(rnv), spe = warp_sum_u64(pe), sfl = warp_sum_u64(fl);
     if (lane == 0) {
         g.tileMaxOverlap[tile] = tileMaxOv;
         g.tileCacheBytes[tile] = tileCache;
         g.tileError[tile] = (uint8_t)tileErr;
-        if (stFE) {
-            atomicAdd((unsigned long long*)&stats[kStFieldEvals], (unsigned long long)stFE);
-            atomicAdd((unsigned long long*)&stats[kStRetained], (unsigned long long)stRNV);
-            atomicAdd((unsigned long long*)&stats[kStPrimEvals], (unsigned long long)stPE);
-            atomicAdd((unsigned long long*)&stats[kStFlops], (unsigned long long)stFL);
+        if (sfe) {
+            atomicAdd(&bs.fe, (unsigned long long)sfe);
+            atomicAdd(&bs.rnv, (unsigned long long)srnv);
+            atomicAdd(&bs.pe, (unsigned long long)spe);
+            atomicAdd(&bs.fl, (unsigned long long)sfl);
         }
-        if (tileMaxOv) atomicMax((unsigned long long*)&stats[kStMaxOverlap], (unsigned long long)tileMaxOv);
-        if (tileCache) atomicMax((unsigned long long*)&stats[kStMaxCache], (unsigned long long)tileCache);
-        if (tileErr) atomicAdd((unsigned long long*)&stats[kStTileErrors], 1ull);
-        if (warpSteps) atomicAdd((unsigned long long*)&stats[kStWarpSteps], (unsigned long long)warpSteps);
+        if (steps) atomicAdd(&bs.steps, (unsigned long long)steps);
+        if (tileErr) atomicAdd(&bs.errs, 1ull);
+        if (tileMaxOv) atomicMax(&bs.maxOv, tileMaxOv);
+        if (tileCache) atomicMax(&bs.maxCache, tileCache);
     }
+    __syncwarp();
 }
 
 // Persistent kernel: each warp pulls tiles from a queue (tiles differ wildly
-// in cost -- empty tiles exit at once) and owns a fixed slot of the fast
-// parameter-block scratch.
+// in cost -- empty tiles exit at once) and owns a fixed slot of the global
+// parameter-block scratch for views too large for its shared memory.
 template <class O, int MinBlocks>
-__global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks) k_trace(DevTree t, Cam cam, TraceParams tp, FrameBufs fb,
-                                                            GBuf g, uint64_t* stats, uint32_t tile0, uint32_t tile1,
-                                                            float4* fastScratch, uint32_t* tileQueue) {
+__global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
+    k_march(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb, GBuf g, uint64_t* stats, uint32_t tile0,
+            uint32_t tile1, float4* fastScratch, uint32_t* tileQueue) {
     extern __shared__ __align__(16) unsigned char smemRaw[];
-    WarpSmem* smem = reinterpret_cast<WarpSmem*>(smemRaw);
+    __shared__ BlockStats bs;
+    MarchSmem* smem = reinterpret_cast<MarchSmem*>(smemRaw);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& s = smem[wid];
-    float4* prm = fastScratch + (size_t)(blockIdx.x * kTraceWarps + wid) * kFastBlockCap;
+    if (threadIdx.x == 0) bs = BlockStats{0, 0, 0, 0, 0, 0, 0u, 0u};
+    __syncthreads();
+    MarchSmem& s = smem[wid];
+    float4* gblk = fastScratch + (size_t)(blockIdx.x * kTraceWarps + wid) * kFastBlockCap;
     for (;;) {
         uint32_t tile = 0;
         if (lane == 0) tile = tile0 + atomicAdd(tileQueue, 1u);
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= tile1) break;
-        trace_tile<O>(t, cam, tp, fb, g, stats, s, prm, lane, tile);
-        __syncwarp();
+        march_tile<O>(t, cam, tp, fb, vb, g, s, gblk, bs, lane, tile);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(stats);
+        if (bs.fe) {
+            atomicAdd(&st[kStFieldEvals], bs.fe);
+            atomicAdd(&st[kStRetained], bs.rnv);
+            atomicAdd(&st[kStPrimEvals], bs.pe);
+            atomicAdd(&st[kStFlops], bs.fl);
+        }
+        if (bs.steps) atomicAdd(&st[kStWarpSteps], bs.steps);
+        if (bs.errs) atomicAdd(&st[kStTileErrors], bs.errs);
+        if (bs.maxOv) atomicMax(&st[kStMaxOverlap], (unsigned long long)bs.maxOv);
+        if (bs.maxCache) atomicMax(&st[kStMaxCache], (unsigned long long)bs.maxCache);
     }
 }
 
@@ -520,11 +552,11 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
 // compiler must fit): a compile-time variant selected once per process
 // ($BT_TRACE_MINBLOCKS, default kDefaultMinBlocks) so the budget can be swept
 // on the device without rebuilding.
-constexpr int kDefaultMinBlocks = 5;  // measured best of {4,5,6,8} on C3
+constexpr int kDefaultMinBlocks = 5;
 
 template <int MB> struct TraceVariant {
     static void* fn(bool exact) {
-        return exact ? (void*)k_trace<ExactOps, MB> : (void*)k_trace<FastOps, MB>;
+        return exact ? (void*)k_march<ExactOps, MB> : (void*)k_march<FastOps, MB>;
     }
 };
 
@@ -552,7 +584,7 @@ void* trace_fn(bool exact) {
 uint32_t trace_grid_blocks(int smCount) {
     static int perSM = 0;
     if (perSM == 0) {
-        const size_t smem = sizeof(WarpSmem) * kTraceWarps;
+        const size_t smem = sizeof(MarchSmem) * kTraceWarps;
         int best = 1;
         for (int ex = 0; ex < 2; ++ex) {
             const void* f = trace_fn(ex != 0);
@@ -570,15 +602,16 @@ size_t trace_scratch_float4s(int smCount) {
     return (size_t)trace_grid_blocks(smCount) * kTraceWarps * kFastBlockCap + 8;
 }
 
-void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
-                  const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats,
-                  uint32_t tile0, uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue) {
+void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
+                  const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
+                  uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue) {
     if (tile1 <= tile0) return;
-    const size_t smem = sizeof(WarpSmem) * kTraceWarps;
-    const uint32_t blocks = std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
+    const size_t smem = sizeof(MarchSmem) * kTraceWarps;
+    const uint32_t blocks =
+        std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
     cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
-    void* args[] = {(void*)&t, (void*)&cam, (void*)&tp, (void*)&fb, (void*)&g, (void*)&stats,
-                    (void*)&tile0, (void*)&tile1, (void*)&fastScratch, (void*)&tileQueue};
+    void* args[] = {(void*)&t,    (void*)&cam,   (void*)&tp,    (void*)&fb,          (void*)&vb,       (void*)&g,
+                    (void*)&stats, (void*)&tile0, (void*)&tile1, (void*)&fastScratch, (void*)&tileQueue};
     cudaLaunchKernel(trace_fn(exact), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
 }
 

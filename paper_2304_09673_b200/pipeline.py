@@ -322,3 +322,10 @@ class Renderer:
         n = np.zeros(4, np.uint32)
         check(self.lib.bt_profile_read(self.ctx, ptr(ms), ptr(n)), "bt_profile_read")
         return ms, n
+
+    def profile_read_ex(self) -> tuple[np.ndarray, np.ndarray]:
+        """[roi_voi, abuffer, trace, normals, views, march] device ms and launch counts."""
+        ms = np.zeros(6, np.float32)
+        n = np.zeros(6, np.uint32)
+        check(self.lib.bt_profile_read_ex(self.ctx, ptr(ms), ptr(n), 6), "bt_profile_read_ex")
+        return ms, n
