@@ -134,8 +134,7 @@ uint32_t view_scan_blocks(uint32_t tiles);
 // ---- launchers (k_trace.cu) -------------------------------------------
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
-                  uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue);
-size_t trace_scratch_float4s(int smCount);
+                  uint32_t tile1, int smCount, uint32_t* tileQueue);
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps);

@@ -119,7 +119,6 @@ struct bt_ctx {
     DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
     DevBuf<IntervalRec> vIv;
     DevBuf<uint32_t> vCounters;
-    DevBuf<float4> traceScratch;  // per-warp fast parameter blocks of k_march (views too large for smem)
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
@@ -380,8 +379,7 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
 // replay an overflow is flagged (bt_stats_download) and the tiles marked.
 int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
              int exact, bool checked) {
-    if (c->traceScratch.cap == 0) {
-        BT_CUDA(c->traceScratch.reserve(trace_scratch_float4s(c->smCount)));
+    if (c->tileQueue.cap == 0) {
         BT_CUDA(c->tileQueue.reserve(1));
         c->bufEpoch++;
     }
@@ -413,7 +411,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
     if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
     launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), view_bufs(c), gbuf(c), c->stats.ptr, tile0, tile1,
-                 c->smCount, c->traceScratch.ptr, c->tileQueue.ptr);
+                 c->smCount, c->tileQueue.ptr);
     if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
         cudaEventSynchronize(c->ev[1]);
@@ -520,7 +518,6 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->normal.release();
     c->stats.release();
     c->gradScratch.release();
-    c->traceScratch.release();
     for (auto* b : {&c->vCount, &c->vLocal, &c->vBlockSum, &c->vBlockPrefix, &c->vNodes}) b->release();
     c->vIv.release();
     c->vCounters.release();

@@ -80,7 +80,7 @@ struct BlockStats {
 // March the pending rays of one interval over the staged view.
 template <class O>
 __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam, const TraceParams& tp, MarchSmem& s,
-                                               const float4* blk, uint32_t nView, uint32_t nPend, float vz0, float vz1,
+                                               bool fits, uint32_t nView, uint32_t nPend, float vz0, float vz1,
                                                uint32_t lt, uint32_t& fe, uint32_t& fl, uint32_t& steps,
                                                uint32_t flops) {
     uint32_t cursor = 0, ray = kNoRay;
@@ -108,7 +108,8 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
                 ray = s.pend[rank];
                 const float4 r = s.rays[ray];
                 dir = F3{r.x, r.y, r.z};
-                march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w), 0u);
+                if (IsFast<O>::value) march_begin(m, vz0 * r.w, vz1 * r.w, 0u);  // r.w = 1 / dot(dir, forward)
+                else march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w), 0u);
             }
             cursor += __popc(idleMask);
         }
@@ -119,8 +120,8 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
         ++steps;
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
-        if (IsFast<O>::value) eval_view_fast<1>(s.hdr, nView, blk, &p, &v);
-        else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);
+        if (IsFast<O>::value && fits) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
+        else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);  // exact path, or an oversized view
         if (march_phase(m) != 0u) march_consume(m, v, tp);
     }
 }
@@ -130,7 +131,7 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
 template <class O>
 __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
                                            const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
-                                           float4* gblk, BlockStats& bs, int lane, uint32_t tile) {
+                                           BlockStats& bs, int lane, uint32_t tile) {
     const uint32_t lt = lanemask_lt();
     const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
     int px[2], py[2];
@@ -152,8 +153,12 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
         tileErr = 1;  // interval records overflowed in a graph replay (flagged to the host)
     } else if (c.x != 0u) {
         const uint2 o = view_offset(vb, tile);
-        s.rays[lane] = fb.rays[(size_t)tile * 64 + lane];
-        s.rays[lane + 32] = fb.rays[(size_t)tile * 64 + lane + 32];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            float4 r = fb.rays[(size_t)tile * 64 + lane + 32 * j];
+            if (IsFast<O>::value) r.w = FastOps::rcp(r.w);  // t = view z * (1 / dot(dir, forward))
+            s.rays[lane + 32 * j] = r;
+        }
         for (uint32_t k = 0; k < c.x; ++k) {
             if ((found0 & found1) == kFull) break;
             const uint4* rp = reinterpret_cast<const uint4*>(vb.iv + o.x + k);
@@ -173,12 +178,14 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
                 break;
             }
             const uint32_t nView = ra.w & 0xFFFFu, nPrim = ra.w >> 16;
-            float4* blk = rb.w <= kMarchBlocks ? s.blocks : gblk;
+            // fast path: evaluation-ready parameter blocks in shared memory when
+            // the view fits (the common case); otherwise raw parameters
+            const bool fits = rb.w <= kMarchBlocks;
             for (uint32_t i = lane; i < nView; i += 32) {
                 const uint2 nd = vb.nodes[ra.z + i];
                 s.hdr[i] = nd.x;
-                if (IsFast<O>::value) convert_node(nd.x, t.words + nd.y + 1, blk + (nd.x & 0xFFFFu));
-                else s.word[i] = nd.y;
+                s.word[i] = nd.y;
+                if (IsFast<O>::value && fits) convert_node(nd.x, t.words + nd.y + 1, s.blocks + (nd.x & 0xFFFFu));
             }
             // queue of this interval: the tile's unfinished rays, in ray order
             const uint32_t p0 = ~found0, p1 = ~found1;
@@ -188,7 +195,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             __syncwarp();
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
             uint32_t ife = 0, ifl = 0;
-            march_interval<O>(t, cam, tp, s, blk, nView, nPend, vz0, vz1, lt, ife, ifl, steps, rb.z);
+            march_interval<O>(t, cam, tp, s, fits, nView, nPend, vz0, vz1, lt, ife, ifl, steps, rb.z);
             fe += ife;
             fl += ifl;
             rnv += ife * nView;
@@ -229,12 +236,11 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
 }
 
 // Persistent kernel: each warp pulls tiles from a queue (tiles differ wildly
-// in cost -- empty tiles exit at once) and owns a fixed slot of the global
-// parameter-block scratch for views too large for its shared memory.
+// in cost -- empty tiles exit at once).
 template <class O, int MinBlocks>
 __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     k_march(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb, GBuf g, uint64_t* stats, uint32_t tile0,
-            uint32_t tile1, float4* fastScratch, uint32_t* tileQueue) {
+            uint32_t tile1, uint32_t* tileQueue) {
     extern __shared__ __align__(16) unsigned char smemRaw[];
     __shared__ BlockStats bs;
     MarchSmem* smem = reinterpret_cast<MarchSmem*>(smemRaw);
@@ -242,13 +248,12 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     if (threadIdx.x == 0) bs = BlockStats{0, 0, 0, 0, 0, 0, 0u, 0u};
     __syncthreads();
     MarchSmem& s = smem[wid];
-    float4* gblk = fastScratch + (size_t)(blockIdx.x * kTraceWarps + wid) * kFastBlockCap;
     for (;;) {
         uint32_t tile = 0;
         if (lane == 0) tile = tile0 + atomicAdd(tileQueue, 1u);
         tile = __shfl_sync(kFull, tile, 0);
         if (tile >= tile1) break;
-        march_tile<O>(t, cam, tp, fb, vb, g, s, gblk, bs, lane, tile);
+        march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -598,20 +603,16 @@ uint32_t trace_grid_blocks(int smCount) {
     return (uint32_t)(perSM * smCount);
 }
 
-size_t trace_scratch_float4s(int smCount) {
-    return (size_t)trace_grid_blocks(smCount) * kTraceWarps * kFastBlockCap + 8;
-}
-
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
-                  uint32_t tile1, int smCount, float4* fastScratch, uint32_t* tileQueue) {
+                  uint32_t tile1, int smCount, uint32_t* tileQueue) {
     if (tile1 <= tile0) return;
     const size_t smem = sizeof(MarchSmem) * kTraceWarps;
     const uint32_t blocks =
         std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
     cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
     void* args[] = {(void*)&t,    (void*)&cam,   (void*)&tp,    (void*)&fb,          (void*)&vb,       (void*)&g,
-                    (void*)&stats, (void*)&tile0, (void*)&tile1, (void*)&fastScratch, (void*)&tileQueue};
+                    (void*)&stats, (void*)&tile0, (void*)&tile1, (void*)&tileQueue};
     cudaLaunchKernel(trace_fn(exact), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
 }
 
