@@ -207,6 +207,16 @@ BT_API int bt_graph_kernel_count(bt_ctx* ctx, uint32_t* kernels, uint32_t* nodes
 BT_API int bt_gbuffer_download(bt_ctx* ctx, uint8_t* hit, float* depth, float* normal,
                                uint32_t* evalCount, uint32_t* tileMaxOverlap,
                                uint32_t* tileCacheBytes, uint8_t* tileError);
+/* Streaming download: snapshots the G-buffer on the device (in stream order,
+ * ~15 us at 1080p) and copies the snapshot to the caller's PINNED host
+ * buffers on the context's copy stream, so frame N's transfer overlaps frame
+ * N+1's render.  Two snapshot slots are used alternately; the host buffers
+ * hold the frame once bt_download_wait() (or bt_sync()) returns.  Same
+ * arguments as bt_gbuffer_download; null planes are skipped. */
+BT_API int bt_gbuffer_download_async(bt_ctx* ctx, uint8_t* hit, float* depth, float* normal,
+                                     uint32_t* evalCount, uint32_t* tileMaxOverlap,
+                                     uint32_t* tileCacheBytes, uint8_t* tileError);
+BT_API int bt_download_wait(bt_ctx* ctx);
 BT_API int bt_gbuffer_device(bt_ctx* ctx, bt_gbuffer_view* out);
 /* hit/depth planes from the host (compute_normals on a caller's G-buffer) */
 BT_API int bt_gbuffer_upload(bt_ctx* ctx, const bt_camera* cam, const uint8_t* hit, const float* depth);

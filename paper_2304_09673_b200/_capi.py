@@ -92,6 +92,8 @@ PROTOTYPES = {
     "bt_oracle_render": [vp, P(bt_camera), P(bt_render_config), C.c_int],
     "bt_render_frame": [vp, P(bt_camera), P(bt_render_config), u32, u32, C.c_int, C.c_int],
     "bt_gbuffer_download": [vp, vp, vp, vp, vp, vp, vp, vp],
+    "bt_gbuffer_download_async": [vp, vp, vp, vp, vp, vp, vp, vp],
+    "bt_download_wait": [vp],
     "bt_gbuffer_device": [vp, P(bt_gbuffer_view)],
     "bt_gbuffer_upload": [vp, P(bt_camera), vp, vp],
     "bt_stats_download": [vp, P(bt_stats)],

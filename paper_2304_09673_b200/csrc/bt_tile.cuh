@@ -184,42 +184,61 @@ BT_DEV void march_begin(March& m, float t0, float t1, uint32_t slot) {
     march_set_phase(m, 1u);
 }
 
-// One field value consumed (tracer.hpp:115-175).  In every non-overshoot
-// case the march moves to the sample (evalT, v): hit if v <= eps, miss if a
-// main step reached t1, else advance.  Only the overshoot back-off branches.
+// One field value consumed (tracer.hpp:115-175), as straight-line selects.
+//
+// Every outcome of the reference loop body is one of:
+//   accept   the sample (evalT, v) becomes (t, f): phase 1 (f(t0)), phase 3
+//            (back-off sample), a trusted main step, or an overshoot whose
+//            back-off point tb already reaches the saved sphere (then
+//            t = savedT = tn, f = savedF = v and relaxation is back on -- the
+//            same state as a trusted step); then hit if v <= eps, miss if a
+//            main step reached t1, else advance (next step, clamped to t1)
+//   back off an overshoot: save (tn, v), march unrelaxed from tb (phase 3),
+//            or miss when tb lies beyond t1
+// All of it is computed unconditionally and committed by predicates, so a
+// warp whose lanes end, hit, overshoot or step in the same iteration does not
+// diverge.  Only reaching a remembered sphere while backing off (rare) takes
+// the looping slow path.  Arithmetic is the reference's, op for op (exact).
 BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     m.evals++;
-    const bool step = march_phase(m) == 2u;
+    const uint32_t ph = m.st & kPhaseMask;
     const float tn = m.evalT;
-    const bool overshoot = step && (m.st & kRelax) &&
-                           (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v)) || v < -tp.hitEps);
-    if (!overshoot) {
-        const bool hit = v <= tp.hitEps;
-        const bool end = step && tn >= m.t1;
+    const bool main = ph == 2u;
+    const bool relax = (m.st & kRelax) != 0u;
+    const bool ovBase = main && relax && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v)) || v < -tp.hitEps);
+    const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
+    const bool ov = ovBase && !(tb >= tn);
+    const bool acc = !ov;
+    const bool hitNow = acc && v <= tp.hitEps;
+    const bool endNow = acc && !hitNow && main && tn >= m.t1;
+    // advance from the accepted sample
+    const float r = E::mul(v, tp.invL);
+    const float tnA = E::add(tn, smax(relax ? E::mul(tp.relax, r) : r, tp.minStep));
+    const bool beyond = tnA > m.t1;
+    const bool stepOn = acc && !hitNow && !endNow;
+    const bool missAdv = stepOn && (!is_finite(r) || (beyond && tn >= m.t1));
+    const bool savedReach = stepOn && !missAdv && (m.st & kSaved) && tnA >= m.savedT;
+    const bool missOv = ov && tb > m.t1;
+    if (acc) {
         m.t = tn;
         m.f = v;
-        if (hit) march_finish(m, true, tn);
-        else if (end) march_finish(m, false, 0.0f);
-        else march_advance(m, tp);
-        return;
     }
-    // remember the non-overlapping sphere, back off to the safe one
-    m.savedT = tn;
-    m.savedF = v;
-    m.st = (m.st & ~kRelax) | kSaved;
-    const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
-    if (tb >= m.savedT) {
-        m.t = m.savedT;
-        m.f = m.savedF;
-        m.st = (m.st & ~kSaved) | kRelax;
-        if (m.f <= tp.hitEps) march_finish(m, true, m.t);
-        else march_advance(m, tp);
-    } else if (tb > m.t1) {
-        march_finish(m, false, 0.0f);
-    } else {
+    if (ov) {  // back off (phase 3) -- the saved sphere is only used when not missing
+        m.savedT = tn;
+        m.savedF = v;
         m.evalT = tb;
-        march_set_phase(m, 3u);
+        m.st = (m.st & ~(kRelax | kPhaseMask)) | kSaved | 3u;
     }
+    if (stepOn) {
+        m.evalT = beyond ? m.t1 : tnA;
+        m.st = (m.st & ~kPhaseMask) | 2u;
+    }
+    if (hitNow) m.st = (m.st & kSlot1) | kHitFlag;
+    if (endNow || missAdv || missOv) {
+        m.st = m.st & kSlot1;
+        m.t = 0.0f;
+    }
+    if (savedReach) march_advance(m, tp);  // rare: re-run the loop head with the saved-sphere rules
 }
 
 }  // namespace btk

@@ -114,6 +114,13 @@ struct bt_ctx {
     DevBuf<uint32_t> evalCount, tileMaxOverlap, tileCacheBytes, fallback;
     bool haveGbuffer = false;
 
+    // streaming download (bt_gbuffer_download_async): two device snapshot slots
+    cudaStream_t copyStream = nullptr;
+    DevBuf<uint8_t> snap[2];
+    cudaEvent_t evSnap[2] = {}, evCopied[2] = {};
+    bool dlPending[2] = {false, false};
+    int dlSlot = 0;
+
     DevBuf<uint64_t> stats;
     // compiled intervals / pruned views of stage (c) (k_views.cu)
     DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
@@ -523,6 +530,15 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->vCounters.release();
     c->tileQueue.release();
     for (auto& e : c->ev) cudaEventDestroy(e);
+    if (c->copyStream) {
+        cudaStreamSynchronize(c->copyStream);
+        cudaStreamDestroy(c->copyStream);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(c->evSnap[i]);
+            cudaEventDestroy(c->evCopied[i]);
+            c->snap[i].release();
+        }
+    }
     cudaStreamDestroy(c->own);
     delete c;
     return BT_OK;
@@ -531,6 +547,7 @@ int bt_ctx_destroy(bt_ctx* c) {
 int bt_sync(bt_ctx* c) {
     if (!c) return fail(BT_EINVAL, "ctx is null");
     BT_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
     BT_CUDA(cudaGetLastError());
     return BT_OK;
 }
@@ -1019,6 +1036,53 @@ int bt_gbuffer_download(bt_ctx* c, uint8_t* hit, float* depth, float* normal, ui
         BT_CUDA(cudaMemcpyAsync(tileCacheBytes, c->tileCacheBytes.ptr, tiles * 4, cudaMemcpyDeviceToHost, s));
     if (tileError) BT_CUDA(cudaMemcpyAsync(tileError, c->tileError.ptr, tiles, cudaMemcpyDeviceToHost, s));
     BT_CUDA(cudaStreamSynchronize(s));
+    BT_CUDA(cudaGetLastError());
+    return BT_OK;
+}
+
+int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
+                              uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
+    // plane layout of a snapshot slot (16-byte aligned offsets)
+    const size_t sz[7] = {px, px * 4, px * 12, px * 4, tiles * 4, tiles * 4, tiles};
+    const void* src[7] = {c->hit.ptr, c->depth.ptr, c->normal.ptr, c->evalCount.ptr,
+                          c->tileMaxOverlap.ptr, c->tileCacheBytes.ptr, c->tileError.ptr};
+    void* dst[7] = {hit, depth, normal, evalCount, tileMaxOverlap, tileCacheBytes, tileError};
+    size_t off[7], total = 0;
+    for (int i = 0; i < 7; ++i) {
+        off[i] = total;
+        total += (sz[i] + 15) & ~(size_t)15;
+    }
+    if (!c->copyStream) {
+        BT_CUDA(cudaStreamCreateWithFlags(&c->copyStream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            BT_CUDA(cudaEventCreateWithFlags(&c->evSnap[i], cudaEventDisableTiming));
+            BT_CUDA(cudaEventCreateWithFlags(&c->evCopied[i], cudaEventDisableTiming));
+        }
+    }
+    const int slot = c->dlSlot;
+    c->dlSlot ^= 1;
+    if (c->dlPending[slot]) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evCopied[slot], 0));  // slot free again
+    if (c->snap[slot].cap < total) {
+        BT_CUDA(cudaStreamSynchronize(c->copyStream));
+        BT_CUDA(c->snap[slot].reserve(total));
+    }
+    uint8_t* base = c->snap[slot].ptr;
+    for (int i = 0; i < 7; ++i)
+        if (dst[i]) BT_CUDA(cudaMemcpyAsync(base + off[i], src[i], sz[i], cudaMemcpyDeviceToDevice, c->stream));
+    BT_CUDA(cudaEventRecord(c->evSnap[slot], c->stream));
+    BT_CUDA(cudaStreamWaitEvent(c->copyStream, c->evSnap[slot], 0));
+    for (int i = 0; i < 7; ++i)
+        if (dst[i]) BT_CUDA(cudaMemcpyAsync(dst[i], base + off[i], sz[i], cudaMemcpyDeviceToHost, c->copyStream));
+    BT_CUDA(cudaEventRecord(c->evCopied[slot], c->copyStream));
+    c->dlPending[slot] = true;
+    return BT_OK;
+}
+
+int bt_download_wait(bt_ctx* c) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
     BT_CUDA(cudaGetLastError());
     return BT_OK;
 }

@@ -7,6 +7,6 @@ import json,sys
 mb=sys.argv[1]
 for l in open(f"gpurun_out/sweep_mb{mb}.txt"):
     if l.startswith("{"):
-        d=json.loads(l); print("minblocks", mb, "frame_ms", d["ms_per_step"], "trace_ms", d["stages_ms"]["trace"], "util", d["frame_stats"]["laneUtilisation"], "frac", d["roofline"]["frac"])
+        d=json.loads(l); print("minblocks", mb, "frame_ms", d["ms_per_step"], "trace_ms", d["stages_ms"]["trace"], "march_ms", d["stages_ms"]["trace_march"], "util", d["frame_stats"]["laneUtilisation"], "frac", d["roofline"]["frac"])
 PY
 done
