@@ -217,6 +217,14 @@ BT_API int bt_gbuffer_download_async(bt_ctx* ctx, uint8_t* hit, float* depth, fl
                                      uint32_t* evalCount, uint32_t* tileMaxOverlap,
                                      uint32_t* tileCacheBytes, uint8_t* tileError);
 BT_API int bt_download_wait(bt_ctx* ctx);
+/* March scheduling.  The persistent march kernel ends with its slowest tile,
+ * so by default (mode 1) the tiles are queued longest-first by a cost proxy
+ * computed with the interval count (fragments and their depth extent;
+ * counting sort on the device, 3 small kernels).  Mode 0: raster order.
+ * bt_set_tile_order installs a fixed host-given permutation of all tiles
+ * instead (mode 2, full frames).  Results never depend on the order. */
+BT_API int bt_set_scheduling(bt_ctx* ctx, int mode);
+BT_API int bt_set_tile_order(bt_ctx* ctx, const uint32_t* order, uint32_t n);
 BT_API int bt_gbuffer_device(bt_ctx* ctx, bt_gbuffer_view* out);
 /* hit/depth planes from the host (compute_normals on a caller's G-buffer) */
 BT_API int bt_gbuffer_upload(bt_ctx* ctx, const bt_camera* cam, const uint8_t* hit, const float* depth);

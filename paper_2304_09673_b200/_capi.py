@@ -94,6 +94,8 @@ PROTOTYPES = {
     "bt_gbuffer_download": [vp, vp, vp, vp, vp, vp, vp, vp],
     "bt_gbuffer_download_async": [vp, vp, vp, vp, vp, vp, vp, vp],
     "bt_download_wait": [vp],
+    "bt_set_tile_order": [vp, vp, u32],
+    "bt_set_scheduling": [vp, C.c_int],
     "bt_gbuffer_device": [vp, P(bt_gbuffer_view)],
     "bt_gbuffer_upload": [vp, P(bt_camera), vp, vp],
     "bt_stats_download": [vp, P(bt_stats)],

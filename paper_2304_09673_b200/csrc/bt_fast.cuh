@@ -169,72 +169,95 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
     // none of these closed forms produces NaN (the reference filters to 0)
 }
 
-BT_DEV float fast_disp(float a, float b, float k, float k6, float invk) {
-    if (!(k > 0.0f)) return 0.0f;
-    const float ad = fabsf(a - b);
-    if (!(ad < k)) return 0.0f;
-    const float t = 1.0f - ad * invk;
-    return k6 * t * t * t;
+// Operators on the fast path.  FMNMX-based min/max (fminf/fmaxf) instead of
+// the reference's std::min/max select semantics: they differ only for NaN
+// operands and signed zeros, which the tolerance path does not carry (field
+// values here are never NaN).  disp = (k/6) max(1 - |a-b|/k, 0)^3 is written
+// branch-free: |a-b| >= k gives t = 0, k = 0 gives t = 0 via fmaxf(NaN, 0).
+BT_DEV float fast_disp(float a, float b, float k6, float invk) {
+    const float t = fmaxf(fmaf(-fabsf(a - b), invk, 1.0f), 0.0f);
+    return k6 * (t * t * t);
 }
 
-BT_DEV float fast_smooth(uint32_t fl, float f0, float f1, float k, float k6, float invk) {
-    float v;
-    if (fl == 0u) v = smin(f0, f1) - fast_disp(f0, f1, k, k6, invk);
-    else if (fl == 1u) v = smax(f0, f1) + fast_disp(f0, f1, k, k6, invk);
-    else v = smax(f0, -f1) + fast_disp(f0, -f1, k, k6, invk);
-    return is_nan(v) ? 0.0f : v;
+BT_DEV float fast_smooth(uint32_t fl, float f0, float f1, float k6, float invk) {
+    if (fl == 0u) return fminf(f0, f1) - fast_disp(f0, f1, k6, invk);
+    if (fl == 1u) return fmaxf(f0, f1) + fast_disp(f0, f1, k6, invk);
+    return fmaxf(f0, -f1) + fast_disp(f0, -f1, k6, invk);
 }
 
+BT_DEV float fast_csg(uint32_t fl, float f0, float f1) {
+    return fl == 0u ? fminf(f0, f1) : (fl == 1u ? fmaxf(f0, f1) : fmaxf(f0, -f1));
+}
+
+// compact_op (field.cpp:424-440): CSG outside the support d, else a smooth
+// blend whose radius shrinks with the smoothed value (blend_range).
+// B[0] = (k, d, k/6, 1/k), B[1].x = 6 / (6d - k).
 BT_DEV float fast_compact(uint32_t fl, const float4* B, float f0, float f1) {
     const float4 b0 = B[0];
-    const float k = b0.x, d = b0.y;
-    if (f0 > d || f1 > d) return csg_op(fl, f0, f1);
-    const float g = fast_smooth(fl, f0, f1, k, b0.z, b0.w);
+    if (fmaxf(f0, f1) > b0.y) return fast_csg(fl, f0, f1);
+    const float g = fast_smooth(fl, f0, f1, b0.z, b0.w);
     const float x = fl == 2u ? fabsf(g) : g;
-    float br = k * smax(1.0f - x * B[1].x, 0.0f);
-    br = is_nan(br) ? 0.0f : br;
-    const float kp = fl == 0u ? br : smin(br, k);
-    return fast_smooth(fl, f0, f1, kp, kp * (1.0f / 6.0f), FastOps::rcp(kp));
+    const float br = b0.x * fmaxf(fmaf(-x, B[1].x, 1.0f), 0.0f);
+    const float kp = fl == 0u ? br : fminf(br, b0.x);
+    return fast_smooth(fl, f0, f1, kp * (1.0f / 6.0f), FastOps::rcp(kp));
 }
 
 // compare chain ordered by frequency (sharp and compact unions dominate
 // blobtree views) instead of an indirect jump table
 BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
     if (code == 9u) return fast_compact(0u, B, f0, f1);
-    if (code == 3u) return smin(f0, f1);
+    if (code == 3u) return fminf(f0, f1);
     if (code >= 10u) return fast_compact(code - 9u, B, f0, f1);
     if (code >= 6u) {
         const float4 b0 = B[0];
-        return fast_smooth(code - 6u, f0, f1, b0.x, b0.y, b0.z);
+        return fast_smooth(code - 6u, f0, f1, b0.y, b0.z);
     }
-    if (code == 4u) return smax(f0, f1);
-    if (code == 5u) return smax(f0, -f1);
+    if (code == 4u) return fmaxf(f0, f1);
+    if (code == 5u) return fmaxf(f0, -f1);
     return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
 }
 
-// Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks,
-// normally in this warp's shared memory), at NP points per lane.
+// Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks in
+// this warp's shared memory), at NP points per lane.  The two top stack
+// entries live in registers (t0 = top, t1 = second): a left comb -- the
+// common blobtree shape -- never touches the local-memory part, deeper
+// entries spill to it only when a third value is pushed.
 template <int NP>
 BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, const F3* p, float* out) {
-    float stk[NP][kStackCap];
+    float deep[NP][kStackCap];
+    float t0[NP], t1[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) t0[k] = t1[k] = 0.0f;
     uint32_t sp = 0;
     for (uint32_t i = 0; i < n; ++i) {
         const uint32_t b = hdr[i];
-        const float4* B = prm + (b & 0xFFFFu);
+        const float4* B = prm + (b & 0xFFFu);
         if (blob_is_prim(b)) {
             float v[NP];
             fast_primitive<NP>(blob_op(b), B, p, v);
+            if (sp >= 2u) {
 #pragma unroll
-            for (int k = 0; k < NP; ++k) stk[k][sp] = v[k];
+                for (int k = 0; k < NP; ++k) deep[k][sp - 2u] = t1[k];
+            }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                t1[k] = t0[k];
+                t0[k] = v[k];
+            }
             ++sp;
         } else {
+            const uint32_t code = blob_op(b);
 #pragma unroll
-            for (int k = 0; k < NP; ++k) stk[k][sp - 2] = fast_operator(blob_op(b), B, stk[k][sp - 2], stk[k][sp - 1]);
+            for (int k = 0; k < NP; ++k) t0[k] = fast_operator(code, B, t1[k], t0[k]);
             --sp;
+            if (sp >= 2u) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) t1[k] = deep[k][sp - 2u];
+            }
         }
     }
 #pragma unroll
-    for (int k = 0; k < NP; ++k) out[k] = stk[k][0];
+    for (int k = 0; k < NP; ++k) out[k] = t0[k];
 }
 
 }  // namespace btk

@@ -50,6 +50,8 @@ struct ViewBufs {
     IntervalRec* iv = nullptr;     // [ivCap]
     uint2* nodes = nullptr;        // [nodeCap] (hdr, word)
     uint32_t* counters = nullptr;  // [0] scan completion, [1] overflow flag
+    const uint32_t* order = nullptr;  // optional march order of the tiles of [tile0, tile1), else raster order
+    uint32_t* tileCost = nullptr;     // [tiles] march cost proxy 0..255 (k_view_count; scheduling)
     uint64_t ivCap = 0, nodeCap = 0;
 };
 
@@ -183,23 +185,27 @@ BT_DEV void view_append(ViewOut& v, uint32_t blob, uint32_t word, bool copyParam
 }
 
 // sparse_traverse<uint8_t, ViewBuildVisitor> (traversal.hpp:41-117,
-// traversal.cpp:30-99) over the active words (ascending).  Returns rootUsed.
-BT_DEV uint32_t build_view(ViewOut& v, const uint32_t* act, uint32_t n, const float4* words) {
+// traversal.cpp:30-99) over the n active words (ascending), which sit in the
+// .x of v.nodes[n - 1 + i]; the view is written over the same 2n - 1 slots
+// (node m goes to slot m <= 2i + 1 < n - 1 + (i + 1) while active i + 1 is
+// still unread).  Returns rootUsed.
+BT_DEV uint32_t build_view_inplace(ViewOut& v, uint32_t n, const float4* words) {
     v.nView = v.nPrim = v.nBlocks = v.cacheFloats = v.depth = v.maxDepth = v.err = 0;
     v.flops = 12u;
     if (n == 0) return 0u;
     v.capacity = 2u * n - 1u;
+    const uint2* act2 = v.nodes + (n - 1u);
     uint32_t sBlob[kStackCap];
     uint8_t sUse[kStackCap];
     uint32_t sp = 0;
     for (uint32_t i = 0; i < n && !v.err; ++i) {
-        const uint32_t w = act[i];
+        const uint32_t w = act2[i].x;
         uint32_t nodeBlob = tree_blob(words, w);
         view_append(v, nodeBlob, w, true);  // visitor.primitive
         v.nPrim++;
         uint32_t data = 1u;
         if (sp > 0) nodeBlob = blob_with_anc(nodeBlob, min(blob_anc(nodeBlob), blob_anc(sBlob[sp - 1])));
-        const uint32_t nextAct = (i + 1 < n) ? act[i + 1] : 0u;
+        const uint32_t nextAct = (i + 1 < n) ? act2[i + 1].x : 0u;
         for (;;) {
             const uint32_t anc = blob_anc(nodeBlob);
             const bool shadowed = (i + 1 < n) && anc > nextAct;

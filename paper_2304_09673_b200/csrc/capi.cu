@@ -126,6 +126,9 @@ struct bt_ctx {
     DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
     DevBuf<IntervalRec> vIv;
     DevBuf<uint32_t> vCounters;
+    // march scheduling: 0 raster, 1 longest-first by cost proxy (default), 2 host order
+    DevBuf<uint32_t> tileOrder, tileCost, orderHist;
+    int schedMode = 1;
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
@@ -201,6 +204,8 @@ ViewBufs view_bufs(const bt_ctx* c) {
     v.iv = c->vIv.ptr;
     v.nodes = c->vNodes.ptr;
     v.counters = c->vCounters.ptr;
+    v.order = nullptr;  // chosen per trace (do_trace)
+    v.tileCost = c->tileCost.ptr;
     v.ivCap = c->vIv.cap;
     v.nodeCap = c->vNodes.cap;
     return v;
@@ -272,6 +277,10 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->vBlockSum.reserve(nvscan));
     BT_CUDA(c->vBlockPrefix.reserve(nvscan + 1));
     BT_CUDA(c->vCounters.reserve(2));
+    BT_CUDA(c->tileCost.reserve(tiles));
+    BT_CUDA(c->tileOrder.reserve(tiles));
+    BT_CUDA(c->orderHist.reserve(256));
+    if (c->schedMode == 2) c->schedMode = 1;  // a host order no longer matches the image
     c->haveAbuffer = false;
     c->haveRays = false;
     c->haveGbuffer = false;
@@ -401,6 +410,8 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+    if (c->schedMode == 1)  // longest-first march order from the count pass's cost proxy
+        launch_tile_order(c->stream, view_bufs(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1);
     if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
     if (checked) {
         uint2 total{0u, 0u};
@@ -417,7 +428,13 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
     if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
-    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), view_bufs(c), gbuf(c), c->stats.ptr, tile0, tile1,
+    ViewBufs vbm = view_bufs(c);
+    if (c->schedMode == 1) {
+        vbm.order = c->tileOrder.ptr;
+    } else if (c->schedMode == 2 && tile0 == 0 && tile1 == tiles) {
+        vbm.order = c->tileOrder.ptr;
+    }
+    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, gbuf(c), c->stats.ptr, tile0, tile1,
                  c->smCount, c->tileQueue.ptr);
     if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
@@ -528,6 +545,9 @@ int bt_ctx_destroy(bt_ctx* c) {
     for (auto* b : {&c->vCount, &c->vLocal, &c->vBlockSum, &c->vBlockPrefix, &c->vNodes}) b->release();
     c->vIv.release();
     c->vCounters.release();
+    c->tileOrder.release();
+    c->tileCost.release();
+    c->orderHist.release();
     c->tileQueue.release();
     for (auto& e : c->ev) cudaEventDestroy(e);
     if (c->copyStream) {
@@ -1077,6 +1097,30 @@ int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* norm
         if (dst[i]) BT_CUDA(cudaMemcpyAsync(dst[i], base + off[i], sz[i], cudaMemcpyDeviceToHost, c->copyStream));
     BT_CUDA(cudaEventRecord(c->evCopied[slot], c->copyStream));
     c->dlPending[slot] = true;
+    return BT_OK;
+}
+
+int bt_set_tile_order(bt_ctx* c, const uint32_t* order, uint32_t n) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    if (n != tiles || !order) return fail(BT_EINVAL, "tile order must list every tile of the image once");
+    std::vector<uint8_t> seen(tiles, 0);
+    for (uint32_t i = 0; i < n; ++i) {
+        if (order[i] >= tiles || seen[order[i]]) return fail(BT_EINVAL, "tile order is not a permutation");
+        seen[order[i]] = 1;
+    }
+    BT_CUDA(cudaMemcpyAsync(c->tileOrder.ptr, order, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    c->schedMode = 2;
+    c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_set_scheduling(bt_ctx* c, int mode) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (mode != 0 && mode != 1) return fail(BT_EINVAL, "scheduling mode must be 0 (raster) or 1 (longest-first)");
+    c->schedMode = mode;
+    c->bufEpoch++;
     return BT_OK;
 }
 

@@ -249,10 +249,11 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     __syncthreads();
     MarchSmem& s = smem[wid];
     for (;;) {
-        uint32_t tile = 0;
-        if (lane == 0) tile = tile0 + atomicAdd(tileQueue, 1u);
-        tile = __shfl_sync(kFull, tile, 0);
-        if (tile >= tile1) break;
+        uint32_t q = 0;
+        if (lane == 0) q = atomicAdd(tileQueue, 1u);
+        q = __shfl_sync(kFull, q, 0);
+        if (q >= tile1 - tile0) break;
+        const uint32_t tile = vb.order ? vb.order[q] : tile0 + q;
         march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
     __syncthreads();

@@ -5,14 +5,17 @@
 //                  fragment list, counts intervals and bounds the view nodes
 //                  (sum of 2 nAct - 1, the ViewOverflow capacity)
 //   k_view_scan    single-pass exclusive scan of the (intervals, nodes) pairs
-//   k_view_build   thread per tile: fetch_interval again, Algorithm-1 view
-//                  build per interval, records written at the scanned offsets
+//   k_view_fetch   thread per tile: fetch_interval again, writing each
+//                  interval's bounds and active words at the scanned offsets
+//   k_view_build   thread per INTERVAL: Algorithm-1 view build in place
 //
 // The fetch loop is re-run instead of stored because it is a few compares per
 // fragment, while storing the active sets would cost more traffic than it
 // saves.  Tiles outside [tile0, tile1) get no intervals.
 #include "bt_device.h"
 #include "bt_views.cuh"
+
+#include <algorithm>
 
 namespace btk {
 
@@ -40,6 +43,11 @@ __global__ void __launch_bounds__(kViewThreads) k_view_count(Cam cam, TraceParam
                 c.y += 2u * s.nAct - 1u;
             }
         }
+        // march cost proxy for longest-first scheduling: fragment count plus
+        // the summed NDC depth extent of the tile's fragments
+        float span = 0.0f;
+        for (uint32_t i = 0; i < cnt; ++i) span += __ldg(&fb.frags[off + i].zExit) - __ldg(&fb.frags[off + i].zEntry);
+        vb.tileCost[tile] = min(255u, 4u * cnt + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
     }
     vb.count[tile] = c;
 }
@@ -114,8 +122,13 @@ __global__ void __launch_bounds__(1024) k_view_scan(ViewBufs vb, uint32_t tiles)
     }
 }
 
-__global__ void __launch_bounds__(kViewThreads) k_view_build(DevTree t, Cam cam, TraceParams tp, FrameBufs fb,
-                                                             ViewBufs vb, uint32_t tile0, uint32_t tile1) {
+// Thread per tile: replay the fetch sequence and write, per interval, the
+// partial record (zBegin, zEnd, node range, overlap) and its active words.
+// The words go to the LAST nAct slots of the interval's 2 nAct - 1 node
+// slots, so the in-place view build below never overwrites an active word
+// before reading it (after active i at most 2i + 1 nodes are written).
+__global__ void __launch_bounds__(kViewThreads) k_view_fetch(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
+                                                             uint32_t tile0, uint32_t tile1) {
     const uint32_t tile = tile0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (tile >= tile1) return;
     const uint2 c = vb.count[tile];
@@ -125,35 +138,106 @@ __global__ void __launch_bounds__(kViewThreads) k_view_build(DevTree t, Cam cam,
     const uint32_t cnt = fb.offsets[tile + 1] - off;
     TileFetch s;
     fetch_init(s);
-    ViewOut v;
     uint32_t nodeOff = o.y;
     float zb;
     for (uint32_t k = 0; k < c.x && fetch_next(s, fb.frags + off, cnt, cam, tp, zb); ++k) {
-        v.nodes = vb.nodes + nodeOff;
-        const uint32_t rootUsed = build_view(v, s.actWord, s.nAct, t.words);
+        const uint32_t n = s.nAct;
+        uint2* act = vb.nodes + nodeOff + n - 1u;
+        for (uint32_t j = 0; j < n; ++j) act[j].x = s.actWord[j];
+        IntervalRec& r = vb.iv[o.x + k];
+        r.zBegin = zb;
+        r.zEnd = s.zEnd;
+        r.nodeOff = nodeOff;
+        r.actFlags = n;
+        nodeOff += 2u * n - 1u;
+    }
+}
+
+// Thread per interval: Algorithm-1 view build over the interval's active
+// words, written in place; completes the record.  Intervals are independent
+// once their active sets are known, so this pass has no per-tile chain.
+__global__ void __launch_bounds__(128) k_view_build(DevTree t, ViewBufs vb, uint32_t totalSlot) {
+    if (vb.counters[1]) return;
+    const uint32_t total = vb.blockPrefix[totalSlot].x;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        IntervalRec& r = vb.iv[k];
+        const uint32_t n = r.actFlags & 0xFFu;
+        ViewOut v;
+        v.nodes = vb.nodes + r.nodeOff;
+        const uint32_t rootUsed = build_view_inplace(v, n, t.words);
         uint32_t flags = 0u;
         if (v.err) flags |= kIvErr;
         if (rootUsed) flags |= kIvRootUsed;
         if (v.maxDepth > kStackCap) flags |= kIvDepthErr;
-        IntervalRec r;
-        r.zBegin = zb;
-        r.zEnd = s.zEnd;
-        r.nodeOff = nodeOff;
         r.viewPrim = v.nView | (v.nPrim << 16);
-        r.actFlags = s.nAct | (flags << 8);
+        r.actFlags = n | (flags << 8);
         r.cacheBytes = v.cacheFloats * 4u;
         r.flops = v.flops;
         r.nBlocks = v.nBlocks;
-        uint4* dst = reinterpret_cast<uint4*>(vb.iv + o.x + k);
-        const uint4* src = reinterpret_cast<const uint4*>(&r);
-        dst[0] = src[0];
-        dst[1] = src[1];
-        nodeOff += 2u * s.nAct - 1u;
-        if (v.err) break;  // the reference's tile loop ends at the first throw
     }
 }
 
+// ---------------------------------------------------------------- scheduling
+// Longest-first order for the march: the persistent march kernel ends when
+// its slowest tile does, so tiles are queued by a cost proxy known before the
+// march (k_view_count: 4 x fragments + 16 x summed NDC depth extent, which
+// tracks the per-tile march steps; measured on C2/C3/C5 it recovers most of
+// the gain of an oracle order).  Counting sort on the proxy (256 bins),
+// descending; equal keys in any order -- the order never changes results.
+constexpr uint32_t kOrderBins = 256;
+
+__device__ __forceinline__ uint32_t order_key(const ViewBufs& vb, uint32_t tile) {
+    return kOrderBins - 1u - min(vb.tileCost[tile], kOrderBins - 1u);  // ascending key = descending cost
+}
+
+__global__ void k_order_count(ViewBufs vb, uint32_t* hist, uint32_t tile0, uint32_t tile1) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t tile = tile0 + i;
+    const uint32_t key = tile < tile1 ? order_key(vb, tile) : kOrderBins;
+    const uint32_t peers = __match_any_sync(kFull, key);
+    if (key < kOrderBins && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
+}
+
+__global__ void __launch_bounds__(kOrderBins) k_order_scan(uint32_t* hist) {
+    __shared__ uint32_t warpSums[kOrderBins / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint32_t v = hist[t];
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += n;
+    }
+    if (lane == 31) warpSums[w] = incl;
+    __syncthreads();
+    uint32_t base = 0;
+    for (int k = 0; k < w; ++k) base += warpSums[k];
+    hist[t] = base + incl - v;  // exclusive start of the bin = its scatter cursor
+}
+
+__global__ void k_order_scatter(ViewBufs vb, uint32_t* cursor, uint32_t* order, uint32_t tile0, uint32_t tile1) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t tile = tile0 + i;
+    const uint32_t key = tile < tile1 ? order_key(vb, tile) : kOrderBins;
+    const uint32_t peers = __match_any_sync(kFull, key);
+    const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (key < kOrderBins && lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    if (key < kOrderBins) order[base + __popc(peers & ((1u << lane) - 1u))] = tile;
+}
+
 }  // namespace
+
+void launch_tile_order(cudaStream_t st, const ViewBufs& vb, uint32_t* hist, uint32_t* order, uint32_t tile0,
+                       uint32_t tile1) {
+    if (tile1 <= tile0) return;
+    const uint32_t n = tile1 - tile0, blocks = (n + 255) / 256;
+    cudaMemsetAsync(hist, 0, kOrderBins * sizeof(uint32_t), st);
+    k_order_count<<<blocks, 256, 0, st>>>(vb, hist, tile0, tile1);
+    k_order_scan<<<1, kOrderBins, 0, st>>>(hist);
+    k_order_scatter<<<blocks, 256, 0, st>>>(vb, hist, order, tile0, tile1);
+}
 
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
                   const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build) {
@@ -166,8 +250,10 @@ void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const Trace
         return;
     }
     if (tile1 > tile0)
-        k_view_build<<<(tile1 - tile0 + kViewThreads - 1) / kViewThreads, kViewThreads, 0, st>>>(t, cam, tp, fb, vb,
+        k_view_fetch<<<(tile1 - tile0 + kViewThreads - 1) / kViewThreads, kViewThreads, 0, st>>>(cam, tp, fb, vb,
                                                                                                  tile0, tile1);
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((vb.ivCap + 127) / 128, 148u * 16u);
+    k_view_build<<<blocks, 128, 0, st>>>(t, vb, (tiles + kViewScanBlock - 1) / kViewScanBlock);
 }
 
 uint32_t view_scan_blocks(uint32_t tiles) { return (tiles + kViewScanBlock - 1) / kViewScanBlock; }

@@ -230,3 +230,36 @@ def test_streaming_download_matches_blocking_download(rd):
         assert out[4].numpy().tobytes() == g.tileMaxOverlap.tobytes()
         assert out[6].numpy().tobytes() == g.tileError.tobytes()
     assert any(a.depth.tobytes() != b.depth.tobytes() for a, b in zip(reference, reference[1:])), "frames differ"
+
+
+def test_march_schedule_never_changes_results(rd):
+    """Raster order, the device's longest-first order (mode 1, after a frame
+    that measured the tile costs) and a random host permutation give
+    bit-identical frames and statistics (tiles are independent)."""
+    import ctypes as C
+    cfg = RenderConfig()
+    s = Scene.build("C3")
+    rd.upload(s)
+    cam = s.device_camera
+    outs = []
+    for mode in ("raster", "lpt", "random"):
+        if mode == "raster":
+            assert rd.lib.bt_set_scheduling(rd.ctx, 0) == 0
+        elif mode == "lpt":
+            assert rd.lib.bt_set_scheduling(rd.ctx, 1) == 0
+            rd.render_frame(cam, cfg, exact=True, graph=False)  # measures the tile costs
+        else:
+            tx, ty = s.tiles
+            perm = np.random.default_rng(7).permutation(tx * ty).astype(np.uint32)
+            assert rd.lib.bt_set_tile_order(rd.ctx, perm.ctypes.data_as(C.c_void_p), len(perm)) == 0
+        rd.reset_stats()
+        rd.render_frame(cam, cfg, exact=True, graph=False)
+        st = rd.stats()
+        outs.append((rd.download_gbuffer(), (st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals,
+                                             st.maxOverlap, st.maxCacheBytes, st.tileErrors, st.warpSteps)))
+    assert rd.lib.bt_set_scheduling(rd.ctx, 1) == 0
+    base, bst = outs[0]
+    for g, st in outs[1:]:
+        assert st == bst
+        for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+            assert getattr(g, plane).tobytes() == getattr(base, plane).tobytes(), plane
