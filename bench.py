@@ -284,6 +284,26 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "work": f"{flops_per_frame / 1e9:.3f} GFLOP/frame algorithmic (SURVEY.md appendix B), "
                 f"{st.fieldEvals} field evals/frame",
     }
+    traffic_path = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(traffic_path):  # dram read+write bytes of one k_march launch (ncu --set full, committed)
+        tr = json.load(open(traffic_path)).get("k_march")
+        if tr:
+            result["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
+            result["roofline"]["traffic_source"] = tr["source"]
+    # (b) A-buffer build, HBM-bound by SURVEY.md 8(d): algorithmic bytes =
+    # V x 64 (volumes read) + T x 8 (CSR offset + count) + F x 12 (fragments written)
+    hbm = None
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        hbm = json.load(open(peaks_path)).get("hbm_gbs")
+    ab_bytes = nprim * 64 + tiles_x * tiles_y * 8 + st.fragments * 12
+    ab_gbs = ab_bytes / (stage_ms["abuffer"] * 1e-3) / 1e9
+    result["abuffer_roofline"] = {
+        "kernels": "k_pairs, k_tiles, k_raster, k_scan, k_scatter, k_sort", "bound": "hbm",
+        "achieved": round(ab_gbs, 2), "peak": hbm, "unit": "GB/s",
+        "frac": round(ab_gbs / hbm, 5) if hbm else None, "algorithmic_bytes": ab_bytes,
+        "note": "latency/IEEE-division bound at these sizes: the algorithmic traffic is ~2 MB per frame",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-written)"}
     result["frame_stats"] = {"fieldEvals": st.fieldEvals, "warpSteps": st.warpSteps,
                              "laneUtilisation": round(st.fieldEvals / max(1, 32 * st.warpSteps), 4),
                              "fragments": st.fragments,

@@ -130,9 +130,12 @@ void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t t
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
                   const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build);
 uint32_t view_scan_blocks(uint32_t tiles);
-// longest-first march order of [tile0, tile1) from vb.tileCost (256-bin histogram scratch)
-void launch_tile_order(cudaStream_t st, const ViewBufs& vb, uint32_t* hist, uint32_t* order, uint32_t tile0,
-                       uint32_t tile1);
+// longest-first march units of [tile0, tile1) from vb.tileCost (hist: 258 words of
+// scratch, [257] = unit count); tiles costing >= beta x the average work per
+// warp (at most cap of them) become two half-tile units
+void launch_tile_order(cudaStream_t st, const ViewBufs& vb, const GBuf& g, uint32_t* hist, uint32_t* order,
+                       uint32_t tile0, uint32_t tile1, uint32_t nWarps, float beta, uint32_t cap);
+uint32_t trace_grid_warps(int smCount);
 
 // ---- launchers (k_trace.cu) -------------------------------------------
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,

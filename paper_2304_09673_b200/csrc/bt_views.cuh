@@ -50,12 +50,16 @@ struct ViewBufs {
     IntervalRec* iv = nullptr;     // [ivCap]
     uint2* nodes = nullptr;        // [nodeCap] (hdr, word)
     uint32_t* counters = nullptr;  // [0] scan completion, [1] overflow flag
-    const uint32_t* order = nullptr;  // optional march order of the tiles of [tile0, tile1), else raster order
+    const uint32_t* order = nullptr;  // optional march units in order (tile | kUnitSplit | kUnitPart1), else raster
+    const uint32_t* unitCount = nullptr;  // number of entries of `order` (device)
     uint32_t* tileCost = nullptr;     // [tiles] march cost proxy 0..255 (k_view_count; scheduling)
     uint64_t ivCap = 0, nodeCap = 0;
 };
 
-constexpr uint32_t kViewScanBlock = 4096;  // tiles per scan block of k_view_scan
+constexpr uint32_t kViewScanBlock = 4096;
+constexpr uint32_t kUnitSplit = 0x80000000u;  // march unit = half a tile (one pixel-column parity)
+constexpr uint32_t kUnitPart1 = 0x40000000u;  // ... the odd columns
+constexpr uint32_t kUnitTile = 0x3FFFFFFFu;  // tiles per scan block of k_view_scan
 
 // exclusive (interval, node) offsets of a tile
 BT_DEV uint2 view_offset(const ViewBufs& vb, uint32_t tile) {

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -127,7 +128,7 @@ struct bt_ctx {
     DevBuf<IntervalRec> vIv;
     DevBuf<uint32_t> vCounters;
     // march scheduling: 0 raster, 1 longest-first by cost proxy (default), 2 host order
-    DevBuf<uint32_t> tileOrder, tileCost, orderHist;
+    DevBuf<uint32_t> tileOrder, tileCost, orderHist, hostUnits;
     int schedMode = 1;
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
@@ -278,8 +279,9 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->vBlockPrefix.reserve(nvscan + 1));
     BT_CUDA(c->vCounters.reserve(2));
     BT_CUDA(c->tileCost.reserve(tiles));
-    BT_CUDA(c->tileOrder.reserve(tiles));
-    BT_CUDA(c->orderHist.reserve(256));
+    BT_CUDA(c->tileOrder.reserve(tiles * 2));
+    BT_CUDA(c->orderHist.reserve(258));
+    BT_CUDA(c->hostUnits.reserve(1));
     if (c->schedMode == 2) c->schedMode = 1;  // a host order no longer matches the image
     c->haveAbuffer = false;
     c->haveRays = false;
@@ -389,6 +391,19 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
     return BT_OK;
 }
 
+// Half-tile split rule of the march scheduler: tiles whose cost proxy is at
+// least beta x the average work per warp become two units ($BT_SPLIT_BETA,
+// default kSplitBeta), at most 2x the grid's warps of them.
+constexpr float kSplitBeta = 0.5f;
+float split_beta() {
+    static float beta = -1.0f;
+    if (beta < 0.0f) {
+        beta = kSplitBeta;
+        if (const char* e = getenv("BT_SPLIT_BETA")) beta = (float)atof(e);
+    }
+    return beta;
+}
+
 // Stage (c): compile the tiles' intervals and views (count, scan, build), then
 // march.  In `checked` mode the record totals are read back after the scan
 // and the record buffers grown (2x headroom) before the build; inside a graph
@@ -410,8 +425,9 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
-    if (c->schedMode == 1)  // longest-first march order from the count pass's cost proxy
-        launch_tile_order(c->stream, view_bufs(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1);
+    if (c->schedMode == 1)  // longest-first march units from the count pass's cost proxy
+        launch_tile_order(c->stream, view_bufs(c), gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
+                          trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
     if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
     if (checked) {
         uint2 total{0u, 0u};
@@ -431,8 +447,10 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     ViewBufs vbm = view_bufs(c);
     if (c->schedMode == 1) {
         vbm.order = c->tileOrder.ptr;
+        vbm.unitCount = c->orderHist.ptr + 257;
     } else if (c->schedMode == 2 && tile0 == 0 && tile1 == tiles) {
         vbm.order = c->tileOrder.ptr;
+        vbm.unitCount = c->hostUnits.ptr;
     }
     launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, gbuf(c), c->stats.ptr, tile0, tile1,
                  c->smCount, c->tileQueue.ptr);
@@ -547,6 +565,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->vCounters.release();
     c->tileOrder.release();
     c->tileCost.release();
+    c->hostUnits.release();
     c->orderHist.release();
     c->tileQueue.release();
     for (auto& e : c->ev) cudaEventDestroy(e);
@@ -1110,6 +1129,7 @@ int bt_set_tile_order(bt_ctx* c, const uint32_t* order, uint32_t n) {
         seen[order[i]] = 1;
     }
     BT_CUDA(cudaMemcpyAsync(c->tileOrder.ptr, order, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->hostUnits.ptr, &n, 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->schedMode = 2;
     c->bufEpoch++;

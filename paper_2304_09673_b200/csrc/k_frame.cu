@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameB
             if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
             vz0 = smax(vz0, cam.nearZ);
             vz1 = smin(vz1, cam.farZ);
-            entry = smin(entry, ndc_from_view_z(cam, vz0));
-            exitv = smax(exitv, ndc_from_view_z(cam, vz1));
+            entry = smin(entry, vz0);  // view z for now: NDC is applied once per item below
+            exitv = smax(exitv, vz1);
             any = true;
         }
         if (!__any_sync(kFull, any)) {
@@ -354,6 +354,13 @@ __global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameB
             entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
             exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
         }
+        // ndc_from_view_z is monotone non-decreasing in vz (correctly rounded
+        // 1/vz, subtraction and scaling are each monotone), so the min / max
+        // over the rays of ndc(vz) is ndc of the min / max vz -- bit for bit
+        // the reference's per-ray min/max (abuffer.cpp:206-213), with two
+        // divisions per item instead of two per ray.
+        entry = ndc_from_view_z(cam, entry);
+        exitv = ndc_from_view_z(cam, exitv);
         if (lane == 0) {
             fb.pool[it] = make_uint4(tile, item.y, __float_as_uint(entry), __float_as_uint(exitv));
             atomicAdd(&fb.tileCount[tile], 1u);

@@ -131,8 +131,12 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
 template <class O>
 __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
                                            const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
-                                           BlockStats& bs, int lane, uint32_t tile) {
+                                           BlockStats& bs, int lane, uint32_t unit) {
     const uint32_t lt = lanemask_lt();
+    // a unit is a whole tile, or half of one (the rays of one pixel-column parity)
+    const uint32_t tile = unit & kUnitTile;
+    const bool half = (unit & kUnitSplit) != 0u;
+    const uint32_t mine = !half ? kFull : ((unit & kUnitPart1) ? 0xAAAAAAAAu : 0x55555555u);
     const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
     int px[2], py[2];
     bool valid[2];
@@ -145,7 +149,9 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
         s.hit[li] = 0;
         s.evals[li] = 0;
     }
-    uint32_t found0 = ~__ballot_sync(kFull, valid[0]), found1 = ~__ballot_sync(kFull, valid[1]);
+    uint32_t found0 = ~(__ballot_sync(kFull, valid[0]) & mine), found1 = ~(__ballot_sync(kFull, valid[1]) & mine);
+    valid[0] = valid[0] && ((mine >> lane) & 1u);
+    valid[1] = valid[1] && ((mine >> lane) & 1u);
     uint32_t tileMaxOv = 0, tileCache = 0, tileErr = 0;
     uint32_t fe = 0, rnv = 0, pe = 0, fl = 0, steps = 0;
     const uint2 c = vb.count[tile];
@@ -218,9 +224,18 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
     }
     const uint64_t sfe = warp_sum_u64(fe), srnv = warp_sum_u64(rnv), spe = warp_sum_u64(pe), sfl = warp_sum_u64(fl);
     if (lane == 0) {
-        g.tileMaxOverlap[tile] = tileMaxOv;
-        g.tileCacheBytes[tile] = tileCache;
-        g.tileError[tile] = (uint8_t)tileErr;
+        if (!half) {
+            g.tileMaxOverlap[tile] = tileMaxOv;
+            g.tileCacheBytes[tile] = tileCache;
+            g.tileError[tile] = (uint8_t)tileErr;
+        } else {  // both halves walk a prefix of the same intervals: the tile's values are the max
+            if (tileMaxOv) atomicMax(&g.tileMaxOverlap[tile], tileMaxOv);
+            if (tileCache) atomicMax(&g.tileCacheBytes[tile], tileCache);
+            if (tileErr) {
+                g.tileError[tile] = 1;
+                if (atomicExch(&vb.tileCost[tile], 1u) != 0u) tileErr = 0;  // count the tile once
+            }
+        }
         if (sfe) {
             atomicAdd(&bs.fe, (unsigned long long)sfe);
             atomicAdd(&bs.rnv, (unsigned long long)srnv);
@@ -248,11 +263,12 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     if (threadIdx.x == 0) bs = BlockStats{0, 0, 0, 0, 0, 0, 0u, 0u};
     __syncthreads();
     MarchSmem& s = smem[wid];
+    const uint32_t nUnits = vb.order ? *vb.unitCount : tile1 - tile0;
     for (;;) {
         uint32_t q = 0;
         if (lane == 0) q = atomicAdd(tileQueue, 1u);
         q = __shfl_sync(kFull, q, 0);
-        if (q >= tile1 - tile0) break;
+        if (q >= nUnits) break;
         const uint32_t tile = vb.order ? vb.order[q] : tile0 + q;
         march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
@@ -603,6 +619,8 @@ uint32_t trace_grid_blocks(int smCount) {
     }
     return (uint32_t)(perSM * smCount);
 }
+
+uint32_t trace_grid_warps(int smCount) { return trace_grid_blocks(smCount) * kTraceWarps; }
 
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,

@@ -198,45 +198,96 @@ __global__ void k_order_count(ViewBufs vb, uint32_t* hist, uint32_t tile0, uint3
     if (key < kOrderBins && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
 }
 
-__global__ void __launch_bounds__(kOrderBins) k_order_scan(uint32_t* hist) {
+// One CTA: bin starts of the march units.  Expensive tiles are also SPLIT:
+// each becomes two units (odd / even pixel columns) marched by two warps,
+// halving the latency of the tiles that bound the kernel's tail.  A tile is
+// split when its cost proxy is at least `beta` x the average work per warp of
+// the grid (total cost / warps) -- many tiles per warp (large frames) split
+// almost nothing, few tiles per warp (small frames) split the heavy ones --
+// and at most `cap` tiles are split.  hist[256] = first unsplit key,
+// hist[257] = total units.
+__global__ void __launch_bounds__(kOrderBins) k_order_scan(uint32_t* hist, uint32_t nWarps, float beta,
+                                                           uint32_t cap) {
     __shared__ uint32_t warpSums[kOrderBins / 32];
+    __shared__ float costSum[kOrderBins / 32];
+    __shared__ uint32_t splitEnd;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const uint32_t v = hist[t];
-    uint32_t incl = v;
+    auto block_scan = [&](uint32_t v) -> uint32_t {  // inclusive
+        uint32_t incl = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t n = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += n;
-    }
-    if (lane == 31) warpSums[w] = incl;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += n;
+        }
+        __syncthreads();
+        if (lane == 31) warpSums[w] = incl;
+        __syncthreads();
+        uint32_t base = 0;
+        for (int k = 0; k < w; ++k) base += warpSums[k];
+        return base + incl;
+    };
+    const uint32_t v = hist[t];
+    const float cost = (float)(kOrderBins - 1 - t);
+    float c = (float)v * cost;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0) costSum[w] = c;
+    if (t == 0) splitEnd = 0;
     __syncthreads();
-    uint32_t base = 0;
-    for (int k = 0; k < w; ++k) base += warpSums[k];
-    hist[t] = base + incl - v;  // exclusive start of the bin = its scatter cursor
+    float total = 0.0f;
+    for (int k = 0; k < (int)(kOrderBins / 32); ++k) total += costSum[k];
+    const uint32_t incl = block_scan(v);
+    // bins 0..splitEnd-1 are split (a prefix: costs decrease with the key)
+    if (v > 0 && t < (int)kOrderBins - 1 && cost * (float)nWarps >= beta * total && incl <= cap)
+        atomicMax(&splitEnd, (uint32_t)t + 1u);
+    __syncthreads();
+    const uint32_t units = t < (int)splitEnd ? 2u * v : v;
+    const uint32_t uincl = block_scan(units);
+    hist[t] = uincl - units;  // exclusive start of the bin = its scatter cursor
+    if (t == (int)kOrderBins - 1) {
+        hist[kOrderBins] = splitEnd;
+        hist[kOrderBins + 1] = uincl;
+    }
 }
 
-__global__ void k_order_scatter(ViewBufs vb, uint32_t* cursor, uint32_t* order, uint32_t tile0, uint32_t tile1) {
+__global__ void k_order_scatter(ViewBufs vb, GBuf g, uint32_t* cursor, uint32_t* order, uint32_t tile0,
+                                uint32_t tile1) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t tile = tile0 + i;
     const uint32_t key = tile < tile1 ? order_key(vb, tile) : kOrderBins;
+    const bool split = key < cursor[kOrderBins];
     const uint32_t peers = __match_any_sync(kFull, key);
     const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    const uint32_t per = split ? 2u : 1u;
     uint32_t base = 0;
-    if (key < kOrderBins && lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+    if (key < kOrderBins && lane == leader) base = atomicAdd(&cursor[key], per * __popc(peers));
     base = __shfl_sync(kFull, base, leader);
-    if (key < kOrderBins) order[base + __popc(peers & ((1u << lane) - 1u))] = tile;
+    if (key >= kOrderBins) return;
+    const uint32_t pos = base + per * __popc(peers & ((1u << lane) - 1u));
+    if (split) {
+        order[pos] = tile | kUnitSplit;
+        order[pos + 1] = tile | kUnitSplit | kUnitPart1;
+        // the two halves combine the tile planes with max (k_march); tileCost
+        // becomes the halves' "error counted" flag
+        vb.tileCost[tile] = 0;
+        g.tileMaxOverlap[tile] = 0;
+        g.tileCacheBytes[tile] = 0;
+        g.tileError[tile] = 0;
+    } else {
+        order[pos] = tile;
+    }
 }
 
 }  // namespace
 
-void launch_tile_order(cudaStream_t st, const ViewBufs& vb, uint32_t* hist, uint32_t* order, uint32_t tile0,
-                       uint32_t tile1) {
+void launch_tile_order(cudaStream_t st, const ViewBufs& vb, const GBuf& g, uint32_t* hist, uint32_t* order,
+                       uint32_t tile0, uint32_t tile1, uint32_t nWarps, float beta, uint32_t cap) {
     if (tile1 <= tile0) return;
     const uint32_t n = tile1 - tile0, blocks = (n + 255) / 256;
     cudaMemsetAsync(hist, 0, kOrderBins * sizeof(uint32_t), st);
     k_order_count<<<blocks, 256, 0, st>>>(vb, hist, tile0, tile1);
-    k_order_scan<<<1, kOrderBins, 0, st>>>(hist);
-    k_order_scatter<<<blocks, 256, 0, st>>>(vb, hist, order, tile0, tile1);
+    k_order_scan<<<1, kOrderBins, 0, st>>>(hist, nWarps, beta, cap);
+    k_order_scatter<<<blocks, 256, 0, st>>>(vb, g, hist, order, tile0, tile1);
 }
 
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,

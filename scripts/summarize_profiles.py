@@ -120,6 +120,7 @@ def main():
         for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
             lines.append(f"| `{k}` | {n} | {us / n:.1f} | {us / total * 100:.1f}% |")
     open(os.path.join(PROF, f"{rnd}_{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+    traffic = {}
     for rep in sorted(f for f in os.listdir(OUT) if f.startswith(tag + "_prof_") and f.endswith(".ncu-rep")):
         kern = rep[len(tag) + 6:-8]
         m, u = raw_metrics(os.path.join(OUT, rep))
@@ -136,6 +137,17 @@ def main():
         for s_, e_, k, t in hot_lines(os.path.join(OUT, rep)):
             out.append(f"- {s_:5.1f}% samples, {e_:5.1f}% inst — {k[0]}:{k[1]} `{t}`")
         open(os.path.join(PROF, f"{rnd}_{tag}_{kern}.md"), "w").write("\n".join(out) + "\n")
+        try:
+            rd_, wr_ = float(m["dram__bytes_read.sum"]), float(m["dram__bytes_write.sum"])
+            mul = lambda k: {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(k, "byte"), 1)  # noqa: E731
+            traffic[kern] = {"dram_bytes_per_launch": rd_ * mul("dram__bytes_read.sum") + wr_ * mul("dram__bytes_write.sum"),
+                             "duration_us": float(m.get("gpu__time_duration.sum", "nan")),
+                             "source": f"profiles/{rnd}_{tag}_{kern}.md (ncu --set full)"}
+        except (KeyError, ValueError):
+            pass
+    if traffic:
+        import json as _json
+        open(os.path.join(PROF, "latest_traffic.json"), "w").write(_json.dumps(traffic, indent=1) + "\n")
     print("written to", PROF)
 
 
