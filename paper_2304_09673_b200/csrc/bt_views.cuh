@@ -67,94 +67,231 @@ BT_DEV uint2 view_offset(const ViewBufs& vb, uint32_t tile) {
     return make_uint2(l.x + p.x, l.y + p.y);
 }
 
-// ---------------------------------------------------------------- fetch
+// ---------------------------------------------------------------- warp fetch
+// fetch_interval (tracer.cpp:50-103; TileFetchState, tracer.hpp:62-84),
+// executed by a WARP on one tile: the active set
+// (<= 96 entries, sorted by word) is spread over the lanes (slot k of lane l
+// is active l + 32k), the tile's fragment list is staged in shared memory,
+// and every O(n) step of the serial loop becomes a ballot / shuffle step:
+//   expire   ballot + popc compaction
+//   maxExit  butterfly max
+//   fetch    candidates cursor..cursor+31 tested in parallel against the
+//            prefix max of the exits before them (the loop's running maxExit);
+//            the fetched count is the first failing candidate
+//   insert   rank merge (words are unique within a tile's list)
+// Bit-identical to the serial loop: same compares, same IEEE
+// view_z_from_ndc, and max/min reductions over finite values.
 
-// Per-tile fetch state (TileFetchState, tracer.hpp:62-84), thread-local.
-struct TileFetch {
-    uint32_t actWord[kMaxOverlap];
-    float actEntry[kMaxOverlap];
-    float actExit[kMaxOverlap];
-    uint32_t nAct, cursor;
-    float zEnd;
+constexpr uint32_t kWarpFragStage = 128;  // fragments of a tile list staged per warp
+
+struct WarpFetchSmem {
+    uint32_t fW[kWarpFragStage];
+    float fEn[kWarpFragStage], fEx[kWarpFragStage];
+    uint32_t tW[kMaxOverlap];  // compaction / merge staging
+    float tEn[kMaxOverlap], tEx[kMaxOverlap];
 };
 
-BT_DEV void fetch_init(TileFetch& s) {
-    s.nAct = 0;
-    s.cursor = 0;
-    s.zEnd = 0.0f;
-}
+struct WarpFetch {
+    uint32_t aW[3];
+    float aEn[3], aEx[3];
+    uint32_t n, cursor, cnt, lane;
+    float zEnd;
+    const Frag* list;
+    WarpFetchSmem* sm;
 
-// fetch_interval (tracer.cpp:50-103).  Returns false once the list is
-// exhausted.  Same float bits as the CPU: compares, std::min/max semantics,
-// view_z_from_ndc in exact IEEE ops.
-BT_DEV bool fetch_next(TileFetch& s, const Frag* list, uint32_t cnt, const Cam& cam, const TraceParams& tp,
-                       float& zBeginOut) {
-    // 1. expire actives whose exit lies behind the previous interval end
-    uint32_t n = s.nAct, m = 0;
-    const float zEndPrev = s.zEnd;
-    for (uint32_t i = 0; i < n; ++i) {
-        if (!(s.actExit[i] <= zEndPrev)) {
-            s.actWord[m] = s.actWord[i];
-            s.actEntry[m] = s.actEntry[i];
-            s.actExit[m] = s.actExit[i];
-            ++m;
+    BT_DEV void frag(uint32_t i, uint32_t& w, float& en, float& ex) const {
+        if (i < kWarpFragStage) {
+            w = sm->fW[i];
+            en = sm->fEn[i];
+            ex = sm->fEx[i];
+        } else {
+            w = __ldg(&list[i].word);
+            en = __ldg(&list[i].zEntry);
+            ex = __ldg(&list[i].zExit);
         }
     }
-    const bool expired = m != n;
-    n = m;
-    uint32_t cursor = s.cursor;
-    const bool hasNext = cursor < cnt;
-    if (n == 0 && !hasNext) {
-        s.nAct = 0;
-        return false;
-    }
-    float zBegin = zEndPrev;
-    if (hasNext) zBegin = smax(zEndPrev, __ldg(&list[cursor].zEntry));
-    const float zBeginView = view_z_from_ndc(cam, zBegin);
-    float maxExit = -f_inf();
-    for (uint32_t i = 0; i < n; ++i) maxExit = smax(maxExit, s.actExit[i]);
+    BT_DEV float entry_at(uint32_t i) const { return i < kWarpFragStage ? sm->fEn[i] : __ldg(&list[i].zEntry); }
 
-    uint32_t fetched = 0;
-    while (cursor < cnt) {
-        const Frag* f = list + cursor;
-        const float ce = __ldg(&f->zEntry);
-        if (n != 0) {
-            if (ce > maxExit) break;
-            if (fetched >= tp.maxNew) break;
-            if (n >= tp.maxOverlap) break;
-            if (E::sub(view_z_from_ndc(cam, ce), zBeginView) >= tp.window) break;
+    BT_DEV void init(const Frag* l, uint32_t count, WarpFetchSmem* smem, uint32_t ln) {
+        list = l;
+        cnt = count;
+        sm = smem;
+        lane = ln;
+        n = 0;
+        cursor = 0;
+        zEnd = 0.0f;
+        for (uint32_t i = lane; i < count && i < kWarpFragStage; i += 32) {
+            sm->fW[i] = __ldg(&l[i].word);
+            sm->fEn[i] = __ldg(&l[i].zEntry);
+            sm->fEx[i] = __ldg(&l[i].zExit);
         }
-        const uint32_t cw = __ldg(&f->word);
-        const float cx = __ldg(&f->zExit);
-        // insert keeping ascending word order (lower_bound position)
-        uint32_t pos = n;
-        while (pos > 0 && s.actWord[pos - 1] >= cw) {
-            s.actWord[pos] = s.actWord[pos - 1];
-            s.actEntry[pos] = s.actEntry[pos - 1];
-            s.actExit[pos] = s.actExit[pos - 1];
-            --pos;
+        __syncwarp();
+    }
+
+    // registers <- staging rows [0, m)
+    BT_DEV void reload(uint32_t m) {
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const uint32_t i = lane + 32u * k;
+            if (i < m) {
+                aW[k] = sm->tW[i];
+                aEn[k] = sm->tEn[i];
+                aEx[k] = sm->tEx[i];
+            }
         }
-        s.actWord[pos] = cw;
-        s.actEntry[pos] = ce;
-        s.actExit[pos] = cx;
-        ++n;
-        maxExit = smax(maxExit, cx);
-        ++cursor;
-        ++fetched;
+        __syncwarp();
     }
-    float zEndNew = maxExit;
-    if (cursor < cnt) zEndNew = smin(__ldg(&list[cursor].zEntry), maxExit);
-    if (zEndNew <= zBegin && fetched == 0 && !expired) {
-        float minExit = f_inf();
-        for (uint32_t i = 0; i < n; ++i) minExit = smin(minExit, s.actExit[i]);
-        zEndNew = minExit;
+
+    // Sorted = false keeps the actives in fetch order instead of word order:
+    // the interval bounds and the active counts are the same (they depend
+    // only on the set), which is all the count pass needs.
+    template <bool Sorted>
+    BT_DEV bool next(const Cam& cam, const TraceParams& tp, float& zBeginOut) {
+        constexpr uint32_t kFullMask = 0xFFFFFFFFu;
+        const uint32_t lt = (1u << lane) - 1u;
+        // 1. expire actives whose exit lies behind the previous interval end
+        const float zEndPrev = zEnd;
+        uint32_t keep[3], m = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const uint32_t i = lane + 32u * k;
+            keep[k] = __ballot_sync(kFullMask, i < n && !(aEx[k] <= zEndPrev));
+            m += __popc(keep[k]);
+        }
+        const bool expired = m != n;
+        if (expired) {
+            uint32_t before = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if ((keep[k] >> lane) & 1u) {
+                    const uint32_t pos = before + __popc(keep[k] & lt);
+                    sm->tW[pos] = aW[k];
+                    sm->tEn[pos] = aEn[k];
+                    sm->tEx[pos] = aEx[k];
+                }
+                before += __popc(keep[k]);
+            }
+            reload(m);
+        }
+        n = m;
+        const bool hasNext = cursor < cnt;
+        if (n == 0 && !hasNext) return false;
+        float zBegin = zEndPrev;
+        if (hasNext) zBegin = smax(zEndPrev, entry_at(cursor));
+        const float zBeginView = view_z_from_ndc(cam, zBegin);
+        float maxExit = -f_inf();
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (lane + 32u * k < n) maxExit = fmaxf(maxExit, aEx[k]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxExit = fmaxf(maxExit, __shfl_xor_sync(kFullMask, maxExit, o));
+
+        // 2. fetch, 32 candidates at a time
+        uint32_t fetchedTotal = 0;
+        for (;;) {
+            const uint32_t avail = cnt - cursor;
+            const uint32_t K = avail < 32u ? avail : 32u;
+            uint32_t cw = 0;
+            float ce = 0.0f, cx = -f_inf();
+            bool ok = false;
+            float inclMax = -f_inf();
+            if (lane < K) frag(cursor + lane, cw, ce, cx);
+            // exclusive prefix max of the candidates' exits
+            inclMax = lane < K ? cx : -f_inf();
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float v = __shfl_up_sync(kFullMask, inclMax, o);
+                if (lane >= (uint32_t)o) inclMax = fmaxf(inclMax, v);
+            }
+            float exclMax = __shfl_up_sync(kFullMask, inclMax, 1);
+            if (lane == 0) exclMax = -f_inf();
+            if (lane < K) {
+                const uint32_t nj = n + lane, fj = fetchedTotal + lane;
+                const float mx = fmaxf(maxExit, exclMax);
+                ok = nj == 0u || !(ce > mx || fj >= tp.maxNew || nj >= tp.maxOverlap ||
+                                   E::sub(view_z_from_ndc(cam, ce), zBeginView) >= tp.window);
+            }
+            const uint32_t okMask = __ballot_sync(kFullMask, ok);
+            const uint32_t fetched = (~okMask) ? (uint32_t)(__ffs(~okMask) - 1) : 32u;  // leading ok lanes
+            if (fetched == 0u) break;
+            if (!Sorted) {  // append in fetch order
+                __syncwarp();
+                if (lane < fetched) {
+                    sm->tW[n + lane] = cw;
+                    sm->tEn[n + lane] = ce;
+                    sm->tEx[n + lane] = cx;
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const uint32_t i = lane + 32u * k;
+                    if (i < n) {
+                        sm->tW[i] = aW[k];
+                        sm->tEn[i] = aEn[k];
+                        sm->tEx[i] = aEx[k];
+                    }
+                }
+                maxExit = fmaxf(maxExit, __shfl_sync(kFullMask, inclMax, fetched - 1u));
+                n += fetched;
+                cursor += fetched;
+                fetchedTotal += fetched;
+                reload(n);
+                if (fetched < 32u || cursor >= cnt) break;
+                continue;
+            }
+            // 3. merge the fetched candidates into the word-sorted active set
+            uint32_t rankOld[3] = {0u, 0u, 0u}, rankNew = 0u;
+            for (uint32_t j = 0; j < fetched; ++j) {
+                const uint32_t wj = __shfl_sync(kFullMask, cw, j);
+                uint32_t below = 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const bool valid = lane + 32u * k < n;
+                    if (valid && aW[k] > wj) rankOld[k]++;
+                    below += __popc(__ballot_sync(kFullMask, valid && aW[k] < wj));
+                }
+                if (lane == j) rankNew += below;
+                if (lane < fetched && wj < cw) rankNew++;
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint32_t i = lane + 32u * k;
+                if (i < n) {
+                    const uint32_t pos = i + rankOld[k];
+                    sm->tW[pos] = aW[k];
+                    sm->tEn[pos] = aEn[k];
+                    sm->tEx[pos] = aEx[k];
+                }
+            }
+            if (lane < fetched) {
+                sm->tW[rankNew] = cw;
+                sm->tEn[rankNew] = ce;
+                sm->tEx[rankNew] = cx;
+            }
+            maxExit = fmaxf(maxExit, __shfl_sync(kFullMask, inclMax, fetched - 1u));
+            n += fetched;
+            cursor += fetched;
+            fetchedTotal += fetched;
+            reload(n);
+            if (fetched < 32u || cursor >= cnt) break;
+        }
+        // 4. interval end
+        float zEndNew = maxExit;
+        if (cursor < cnt) zEndNew = smin(entry_at(cursor), maxExit);
+        if (zEndNew <= zBegin && fetchedTotal == 0u && !expired) {
+            float minExit = f_inf();
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (lane + 32u * k < n) minExit = fminf(minExit, aEx[k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) minExit = fminf(minExit, __shfl_xor_sync(kFullMask, minExit, o));
+            zEndNew = minExit;
+        }
+        zEnd = zEndNew;
+        zBeginOut = zBegin;
+        return true;
     }
-    s.nAct = n;
-    s.cursor = cursor;
-    s.zEnd = zEndNew;
-    zBeginOut = zBegin;
-    return true;
-}
+};
 
 // ---------------------------------------------------------------- view build
 

@@ -1,11 +1,11 @@
 // k_views.cu -- stage (c), part 1 on sm_100a: compile every tile's interval
 // sequence and pruned views (see bt_views.cuh for the record format).
 //
-//   k_view_count   thread per tile: runs fetch_interval over the tile's
-//                  fragment list, counts intervals and bounds the view nodes
-//                  (sum of 2 nAct - 1, the ViewOverflow capacity)
+//   k_view_count   warp per tile (WarpFetch): runs fetch_interval over the
+//                  tile's fragment list, counts intervals and bounds the view
+//                  nodes (sum of 2 nAct - 1, the ViewOverflow capacity)
 //   k_view_scan    single-pass exclusive scan of the (intervals, nodes) pairs
-//   k_view_fetch   thread per tile: fetch_interval again, writing each
+//   k_view_fetch   warp per tile: fetch_interval again, writing each
 //                  interval's bounds and active words at the scanned offsets
 //   k_view_build   thread per INTERVAL: Algorithm-1 view build in place
 //
@@ -22,34 +22,41 @@ namespace btk {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kViewThreads = 64;      // small blocks: the tiles of a frame spread over all SMs
+constexpr uint32_t kViewWarps = 4;    // warps (tiles) per block of the fetch passes
 
 __device__ __forceinline__ uint2 add2(uint2 a, uint2 b) { return make_uint2(a.x + b.x, a.y + b.y); }
 
-__global__ void __launch_bounds__(kViewThreads) k_view_count(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
-                                                             uint32_t tile0, uint32_t tile1, uint32_t tiles) {
-    const uint32_t tile = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per tile (WarpFetch): run the fetch sequence, count intervals and the
+// view-node bound; lane 0 also records the scheduling cost proxy.
+__global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
+                                                                uint32_t tile0, uint32_t tile1, uint32_t tiles) {
+    __shared__ WarpFetchSmem sm[kViewWarps];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const uint32_t tile = blockIdx.x * kViewWarps + wid;
     if (tile >= tiles) return;
     uint2 c = make_uint2(0u, 0u);
     if (tile >= tile0 && tile < tile1) {
         const uint32_t off = fb.offsets[tile];
         const uint32_t cnt = fb.offsets[tile + 1] - off;
         if (cnt) {
-            TileFetch s;
-            fetch_init(s);
+            WarpFetch f;
+            f.init(fb.frags + off, cnt, &sm[wid], lane);
             float zb;
-            while (fetch_next(s, fb.frags + off, cnt, cam, tp, zb)) {
+            while (f.next<false>(cam, tp, zb)) {
                 c.x += 1u;
-                c.y += 2u * s.nAct - 1u;
+                c.y += 2u * f.n - 1u;
             }
         }
         // march cost proxy for longest-first scheduling: fragment count plus
         // the summed NDC depth extent of the tile's fragments
         float span = 0.0f;
-        for (uint32_t i = 0; i < cnt; ++i) span += __ldg(&fb.frags[off + i].zExit) - __ldg(&fb.frags[off + i].zEntry);
-        vb.tileCost[tile] = min(255u, 4u * cnt + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
+        for (uint32_t i = lane; i < cnt; i += 32)
+            span += __ldg(&fb.frags[off + i].zExit) - __ldg(&fb.frags[off + i].zEntry);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(kFull, span, o);
+        if (lane == 0) vb.tileCost[tile] = min(255u, 4u * cnt + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
     }
-    vb.count[tile] = c;
+    if (lane == 0) vb.count[tile] = c;
 }
 
 // Same single-pass structure as the A-buffer scan (k_frame.cu): each block
@@ -122,33 +129,39 @@ __global__ void __launch_bounds__(1024) k_view_scan(ViewBufs vb, uint32_t tiles)
     }
 }
 
-// Thread per tile: replay the fetch sequence and write, per interval, the
+// Warp per tile: replay the fetch sequence and write, per interval, the
 // partial record (zBegin, zEnd, node range, overlap) and its active words.
 // The words go to the LAST nAct slots of the interval's 2 nAct - 1 node
 // slots, so the in-place view build below never overwrites an active word
 // before reading it (after active i at most 2i + 1 nodes are written).
-__global__ void __launch_bounds__(kViewThreads) k_view_fetch(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
-                                                             uint32_t tile0, uint32_t tile1) {
-    const uint32_t tile = tile0 + blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kViewWarps * 32) k_view_fetch(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
+                                                                uint32_t tile0, uint32_t tile1) {
+    __shared__ WarpFetchSmem sm[kViewWarps];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const uint32_t tile = tile0 + blockIdx.x * kViewWarps + wid;
     if (tile >= tile1) return;
     const uint2 c = vb.count[tile];
     if (c.x == 0 || vb.counters[1]) return;  // no intervals, or the frame overflowed (march flags it)
     const uint2 o = view_offset(vb, tile);
     const uint32_t off = fb.offsets[tile];
     const uint32_t cnt = fb.offsets[tile + 1] - off;
-    TileFetch s;
-    fetch_init(s);
+    WarpFetch f;
+    f.init(fb.frags + off, cnt, &sm[wid], lane);
     uint32_t nodeOff = o.y;
     float zb;
-    for (uint32_t k = 0; k < c.x && fetch_next(s, fb.frags + off, cnt, cam, tp, zb); ++k) {
-        const uint32_t n = s.nAct;
+    for (uint32_t k = 0; k < c.x && f.next<true>(cam, tp, zb); ++k) {
+        const uint32_t n = f.n;
         uint2* act = vb.nodes + nodeOff + n - 1u;
-        for (uint32_t j = 0; j < n; ++j) act[j].x = s.actWord[j];
-        IntervalRec& r = vb.iv[o.x + k];
-        r.zBegin = zb;
-        r.zEnd = s.zEnd;
-        r.nodeOff = nodeOff;
-        r.actFlags = n;
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+            if (lane + 32u * s < n) act[lane + 32u * s].x = f.aW[s];
+        if (lane == 0) {
+            IntervalRec& r = vb.iv[o.x + k];
+            r.zBegin = zb;
+            r.zEnd = f.zEnd;
+            r.nodeOff = nodeOff;
+            r.actFlags = n;
+        }
         nodeOff += 2u * n - 1u;
     }
 }
@@ -294,15 +307,15 @@ void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const Trace
                   const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build) {
     if (!build) {
         cudaMemsetAsync(vb.counters, 0, 2 * sizeof(uint32_t), st);
-        k_view_count<<<(tiles + kViewThreads - 1) / kViewThreads, kViewThreads, 0, st>>>(cam, tp, fb, vb, tile0,
-                                                                                          tile1, tiles);
+        k_view_count<<<(tiles + kViewWarps - 1) / kViewWarps, kViewWarps * 32, 0, st>>>(cam, tp, fb, vb, tile0,
+                                                                                         tile1, tiles);
         const uint32_t nblocks = (tiles + kViewScanBlock - 1) / kViewScanBlock;
         k_view_scan<<<nblocks, 1024, 0, st>>>(vb, tiles);
         return;
     }
     if (tile1 > tile0)
-        k_view_fetch<<<(tile1 - tile0 + kViewThreads - 1) / kViewThreads, kViewThreads, 0, st>>>(cam, tp, fb, vb,
-                                                                                                 tile0, tile1);
+        k_view_fetch<<<(tile1 - tile0 + kViewWarps - 1) / kViewWarps, kViewWarps * 32, 0, st>>>(cam, tp, fb, vb,
+                                                                                                tile0, tile1);
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((vb.ivCap + 127) / 128, 148u * 16u);
     k_view_build<<<blocks, 128, 0, st>>>(t, vb, (tiles + kViewScanBlock - 1) / kViewScanBlock);
 }
