@@ -5,10 +5,10 @@
 // (tracer.cpp:50-103, traversal.cpp:30-99) with the 64-ray march of each
 // interval (tracer.cpp:155-232).  Neither the intervals nor the views depend
 // on the march -- the march only decides how far down the list a tile goes
-// (it stops once all 64 rays have hit).  So the serial part runs here as one
-// THREAD per tile over the whole list (k_views.cu), 32 tiles per warp instead
-// of one lane of a 32-lane warp, and the march kernel reads the compiled
-// records:
+// (it stops once all 64 rays have hit).  So they are compiled ahead of the
+// march (k_views.cu): a warp per tile replays the fetch sequence with the
+// O(n) steps spread over its lanes, a thread per interval builds the view,
+// and the march kernel reads the records:
 //
 //   IntervalRec (32 B)  zBegin/zEnd (NDC), the view's node range, overlap,
 //                       cache bytes, flags, appendix-B flops, fast-block size
