@@ -147,7 +147,10 @@ def main():
             pass
     if traffic:
         import json as _json
-        open(os.path.join(PROF, "latest_traffic.json"), "w").write(_json.dumps(traffic, indent=1) + "\n")
+        path = os.path.join(PROF, "latest_traffic.json")
+        merged = _json.load(open(path)) if os.path.exists(path) else {}
+        merged.update(traffic)
+        open(path, "w").write(_json.dumps(merged, indent=1) + "\n")
     print("written to", PROF)
 
 
