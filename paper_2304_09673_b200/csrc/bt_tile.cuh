@@ -122,49 +122,6 @@ BT_DEV void march_finish(March& m, bool hit, float t) {
 
 BT_DEV void march_set_phase(March& m, uint32_t ph) { m.st = (m.st & ~kPhaseMask) | ph; }
 
-// Advance without evaluating until a field value is needed (reference loop
-// head, tracer.hpp:115-139: step, saved-sphere reuse, clamp to t1).  The
-// common case is straight-line select code; reusing a saved sample is the
-// rare case and loops.
-BT_DEV void march_advance(March& m, const TraceParams& tp) {
-    for (;;) {
-        const float r = E::mul(m.f, tp.invL);
-        float tn = E::add(m.t, smax((m.st & kRelax) ? E::mul(tp.relax, r) : r, tp.minStep));
-        if (!is_finite(r)) {
-            march_finish(m, false, 0.0f);
-            return;
-        }
-        if ((m.st & kSaved) && tn >= m.savedT) {  // rare: reaching the remembered sphere
-            const bool reuse = m.savedT >= E::add(m.t, tp.minStep) && m.savedT <= m.t1;
-            m.st = (m.st & ~kSaved) | kRelax;
-            if (reuse) {
-                // reused sample: never an overshoot, never beyond t1
-                const float fn = m.savedF;
-                tn = m.savedT;
-                if (fn <= tp.hitEps) {
-                    march_finish(m, true, tn);
-                    return;
-                }
-                if (tn >= m.t1) {
-                    march_finish(m, false, 0.0f);
-                    return;
-                }
-                m.t = tn;
-                m.f = fn;
-                continue;
-            }
-        }
-        const bool beyond = tn > m.t1;
-        if (beyond && m.t >= m.t1) {
-            march_finish(m, false, 0.0f);
-            return;
-        }
-        m.evalT = beyond ? m.t1 : tn;
-        march_set_phase(m, 2u);
-        return;
-    }
-}
-
 BT_DEV void march_idle(March& m, uint32_t slot) {
     m.st = slot ? kSlot1 : 0u;
     m.evals = 0;
@@ -192,36 +149,53 @@ BT_DEV void march_begin(March& m, float t0, float t1, uint32_t slot) {
 //            back-off point tb already reaches the saved sphere (then
 //            t = savedT = tn, f = savedF = v and relaxation is back on -- the
 //            same state as a trusted step); then hit if v <= eps, miss if a
-//            main step reached t1, else advance (next step, clamped to t1)
+//            main step reached t1, else advance: the next step from (t, f),
+//            clamped to t1.  While backing off, an advance that reaches the
+//            remembered sphere re-uses it (no evaluation): hit / miss tests on
+//            (savedT, savedF), then one more relaxed advance from there.
 //   back off an overshoot: save (tn, v), march unrelaxed from tb (phase 3),
 //            or miss when tb lies beyond t1
-// All of it is computed unconditionally and committed by predicates, so a
-// warp whose lanes end, hit, overshoot or step in the same iteration does not
-// diverge.  Only reaching a remembered sphere while backing off (rare) takes
-// the looping slow path.  Arithmetic is the reference's, op for op (exact).
+// Everything is computed unconditionally and committed by predicates, so a
+// warp whose lanes end, hit, overshoot, back off or re-use a sphere in the
+// same iteration never diverges.  Arithmetic is the reference's, op for op.
 BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     m.evals++;
     const uint32_t ph = m.st & kPhaseMask;
     const float tn = m.evalT;
     const bool main = ph == 2u;
     const bool relax = (m.st & kRelax) != 0u;
+    const bool saved = (m.st & kSaved) != 0u;
     const bool ovBase = main && relax && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v)) || v < -tp.hitEps);
     const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
     const bool ov = ovBase && !(tb >= tn);
     const bool acc = !ov;
     const bool hitNow = acc && v <= tp.hitEps;
     const bool endNow = acc && !hitNow && main && tn >= m.t1;
-    // advance from the accepted sample
-    const float r = E::mul(v, tp.invL);
-    const float tnA = E::add(tn, smax(relax ? E::mul(tp.relax, r) : r, tp.minStep));
-    const bool beyond = tnA > m.t1;
     const bool stepOn = acc && !hitNow && !endNow;
-    const bool missAdv = stepOn && (!is_finite(r) || (beyond && tn >= m.t1));
-    const bool savedReach = stepOn && !missAdv && (m.st & kSaved) && tnA >= m.savedT;
+    // advance from the accepted sample (tn, v) with the current relaxation
+    const float r = E::mul(v, tp.invL);
+    const bool fin = is_finite(r);
+    const float tnA = E::add(tn, smax(relax ? E::mul(tp.relax, r) : r, tp.minStep));
+    // ... reaching the remembered sphere while backing off
+    const bool reach = stepOn && fin && saved && tnA >= m.savedT;
+    const bool reuse = reach && m.savedT >= E::add(tn, tp.minStep) && m.savedT <= m.t1;
+    const bool hit2 = reuse && m.savedF <= tp.hitEps;
+    const bool end2 = reuse && !hit2 && m.savedT >= m.t1;
+    const float r2 = E::mul(m.savedF, tp.invL);
+    const float tn2 = E::add(m.savedT, smax(E::mul(tp.relax, r2), tp.minStep));  // relaxation is back on
+    const bool miss2 = reuse && !hit2 && !end2 && !is_finite(r2);
+    const bool step2 = reuse && !hit2 && !end2 && !miss2;
+    const bool beyond = tnA > m.t1;
+    const bool missAdv = stepOn && !reuse && (!fin || (beyond && tn >= m.t1));
+    const bool step1 = stepOn && !reuse && !missAdv;
     const bool missOv = ov && tb > m.t1;
     if (acc) {
         m.t = tn;
         m.f = v;
+    }
+    if (reuse) {
+        m.t = m.savedT;
+        m.f = m.savedF;
     }
     if (ov) {  // back off (phase 3) -- the saved sphere is only used when not missing
         m.savedT = tn;
@@ -229,16 +203,20 @@ BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
         m.evalT = tb;
         m.st = (m.st & ~(kRelax | kPhaseMask)) | kSaved | 3u;
     }
-    if (stepOn) {
+    if (reach) m.st = (m.st & ~kSaved) | kRelax;
+    if (step1) {
         m.evalT = beyond ? m.t1 : tnA;
         m.st = (m.st & ~kPhaseMask) | 2u;
     }
-    if (hitNow) m.st = (m.st & kSlot1) | kHitFlag;
-    if (endNow || missAdv || missOv) {
+    if (step2) {
+        m.evalT = tn2 > m.t1 ? m.t1 : tn2;
+        m.st = (m.st & ~kPhaseMask) | 2u;
+    }
+    if (hitNow || hit2) m.st = (m.st & kSlot1) | kHitFlag;  // t holds the hit (tn or savedT)
+    if (endNow || missAdv || missOv || end2 || miss2) {
         m.st = m.st & kSlot1;
         m.t = 0.0f;
     }
-    if (savedReach) march_advance(m, tp);  // rare: re-run the loop head with the saved-sphere rules
 }
 
 }  // namespace btk

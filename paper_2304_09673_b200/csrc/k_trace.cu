@@ -574,7 +574,7 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
 // compiler must fit): a compile-time variant selected once per process
 // ($BT_TRACE_MINBLOCKS, default kDefaultMinBlocks) so the budget can be swept
 // on the device without rebuilding.
-constexpr int kDefaultMinBlocks = 5;
+constexpr int kDefaultMinBlocks = 6;  // measured best of {4,5,6,8} on C3 (C1, C2 agree; C5 prefers 5 by 2 %)
 
 template <int MB> struct TraceVariant {
     static void* fn(bool exact) {
