@@ -419,7 +419,7 @@ __device__ __forceinline__ void eval_subtree6(const DevTree& t, uint2 range, con
 }
 
 template <class O>
-__global__ void __launch_bounds__(256) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
+__global__ void __launch_bounds__(1024) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
                                                   const uint32_t* counters, uint64_t* stats, float* scratch,
                                                   uint32_t useSmem) {
     extern __shared__ float dyn[];
@@ -650,10 +650,13 @@ void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& ca
         cudaFuncSetAttribute(k_gradient<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemBytes);
         attr = true;
     }
+    // one CTA per queued pixel: as many threads as frontier subtrees (phase 1
+    // is one subtree per thread), at least 6 warps for the min-chain phase
+    const uint32_t threads = std::min<uint32_t>(1024u, std::max<uint32_t>(256u, (t.nFrontier + 31u) & ~31u));
     if (exact)
-        k_gradient<ExactOps><<<scratchWarps, 256, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
+        k_gradient<ExactOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
     else
-        k_gradient<FastOps><<<scratchWarps, 256, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
+        k_gradient<FastOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
 }
 
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
