@@ -64,6 +64,7 @@ enum : int {
     kCntCandidates = 3,
     kCntFallback = 4,
     kCntOverflow = 5,
+    kCntFallbackHard = 6,  // fast-path fallbacks without a usable view (full-tree gradient)
     kCntSlots = 8
 };
 
@@ -141,9 +142,13 @@ uint32_t trace_grid_warps(int smCount);
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
                   uint32_t tile1, int smCount, uint32_t* tileQueue);
+// vb: the interval records of the march that produced this G-buffer (whole
+// frame, FMA path) -- the gradient fallback then evaluates the pruned view
+// of the interval each ray hit in; nullptr: the full tree (reference)
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
-                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps);
+                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
+                    const ViewBufs* vb);
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                    const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats);
 

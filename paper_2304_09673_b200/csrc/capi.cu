@@ -129,6 +129,7 @@ struct bt_ctx {
     DevBuf<uint32_t> vCounters;
     // march scheduling: 0 raster, 1 longest-first by cost proxy (default), 2 host order
     DevBuf<uint32_t> tileOrder, tileCost, orderHist, hostUnits;
+    bool viewsFrame = false;  // the G-buffer came from a whole-frame FMA-path march (its records are valid)
     int schedMode = 1;
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
@@ -467,6 +468,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         c->profLaunch[5] += 1;
     }
     c->haveGbuffer = true;
+    c->viewsFrame = !exact && tile0 == 0 && tile1 == tiles;
     return BT_OK;
 }
 
@@ -486,8 +488,10 @@ int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
         c->gradWarps = (uint32_t)ctas;
         c->bufEpoch++;
     }
+    const ViewBufs vb = view_bufs(c);
     launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
-                   c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps);
+                   c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps,
+                   c->viewsFrame && !exact ? &vb : nullptr);
     return BT_OK;
 }
 
@@ -971,6 +975,7 @@ int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cf
     BT_CUDA(cudaMemsetAsync(c->tileCacheBytes.ptr, 0, c->tileCacheBytes.cap * 4, c->stream));
     BT_CUDA(cudaMemsetAsync(c->tileError.ptr, 0, c->tileError.cap, c->stream));
     c->haveGbuffer = true;
+    c->viewsFrame = false;
     return BT_OK;
 }
 
@@ -1178,6 +1183,7 @@ int bt_gbuffer_upload(bt_ctx* c, const bt_camera* cam, const uint8_t* hit, const
     BT_CUDA(cudaMemcpyAsync(c->hit.ptr, hit, px, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->depth.ptr, depth, px * 4, cudaMemcpyHostToDevice, c->stream));
     c->haveGbuffer = true;
+    c->viewsFrame = false;
     return BT_OK;
 }
 

@@ -421,11 +421,13 @@ __device__ __forceinline__ void eval_subtree6(const DevTree& t, uint2 range, con
 template <class O>
 __global__ void __launch_bounds__(1024) k_gradient(DevTree t, Cam cam, FrameBufs fb, GBuf g,
                                                   const uint32_t* counters, uint64_t* stats, float* scratch,
-                                                  uint32_t useSmem) {
+                                                  uint32_t useSmem, uint32_t hardList) {
     extern __shared__ float dyn[];
     __shared__ float res[6];
-    const uint32_t n = counters[kCntFallback];
-    if (threadIdx.x == 0 && blockIdx.x == 0)
+    // main list: fallback[0, n); the fast path's hard list: fallback[px - 1 - i]
+    const uint32_t n = counters[hardList ? kCntFallbackHard : kCntFallback];
+    const uint32_t px = (uint32_t)g.width * (uint32_t)g.height;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && !hardList)
         atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
     float* vals = useSmem ? dyn : scratch + (size_t)blockIdx.x * t.nFrontier * 6;
     // the serial upper program is staged once into shared memory (its loads
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(1024) k_gradient(DevTree t, Cam cam, FrameBufs
         __syncthreads();
     }
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const uint32_t p = g.fallback[i];
+        const uint32_t p = g.fallback[hardList ? px - 1u - i : i];
         const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
         const F3 pc = position_at(cam, fb, g, x, y);
         const float h = smax(1e-3f, E::mul(1e-4f, g.depth[p]));
@@ -532,6 +534,85 @@ __global__ void __launch_bounds__(1024) k_gradient(DevTree t, Cam cam, FrameBufs
             g.normal[3 * p + 2] = nn.z;
         }
         __syncthreads();
+    }
+}
+
+// Tolerance path of the gradient fallback: eval_full is replaced by the
+// pruned view of the interval the ray hit in (the march's own records), one
+// warp per pixel, lanes 0..5 one tap each.  Near the hit every primitive
+// whose volume of interest reaches the point is in that view, so the field
+// agrees with eval_full there to ~1 ulp (the reference's own pruned-vs-full
+// bound, test_traversal.cpp:132-152) -- at the cost of one small view per
+// tap instead of the whole tree.  Pixels without a usable interval go to the
+// hard list (full tree).
+constexpr int kGradViewWarps = 4;
+__global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t, Cam cam, FrameBufs fb, ViewBufs vb,
+                                                                        GBuf g, uint32_t* counters, uint64_t* stats) {
+    __shared__ uint32_t sh[kGradViewWarps][kViewCap], sw[kGradViewWarps][kViewCap];
+    __shared__ float res[kGradViewWarps][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t n = counters[kCntFallback];
+    const uint32_t px = (uint32_t)g.width * (uint32_t)g.height;
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        atomicAdd((unsigned long long*)&stats[kStFallbacks], (unsigned long long)n);
+    const uint32_t nwarps = gridDim.x * kGradViewWarps;
+    for (uint32_t i = blockIdx.x * kGradViewWarps + w; i < n; i += nwarps) {
+        const uint32_t p = g.fallback[i];
+        const int x = (int)(p % (uint32_t)g.width), y = (int)(p / (uint32_t)g.width);
+        const uint32_t tile = (uint32_t)((y >> 3) * g.tilesX + (x >> 3));
+        const float4 r = fb.rays[(size_t)tile * 64 + ((y & 7) << 3) + (x & 7)];
+        const float depth = g.depth[p];
+        const float z = ndc_from_view_z(cam, E::mul(depth, r.w));
+        // the first usable interval containing the hit, else the last one starting before it
+        const uint32_t cnt = vb.counters[1] ? 0u : vb.count[tile].x;
+        const uint2 o = cnt ? view_offset(vb, tile) : make_uint2(0u, 0u);
+        int first = -1, last = -1;
+        for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            bool c1 = false, c2 = false;
+            if (k < cnt) {
+                const IntervalRec rec = vb.iv[o.x + k];
+                const uint32_t fl = rec.actFlags >> 8;
+                const bool ok = (fl & kIvRootUsed) && !(fl & (kIvErr | kIvDepthErr));
+                c2 = ok && rec.zBegin <= z;
+                c1 = c2 && z <= rec.zEnd;
+            }
+            const uint32_t m1 = __ballot_sync(kFull, c1), m2 = __ballot_sync(kFull, c2);
+            if (m1 && first < 0) first = (int)k0 + __ffs(m1) - 1;
+            if (m2) last = (int)k0 + 31 - __clz(m2);
+        }
+        const int sel = first >= 0 ? first : last;
+        if (sel < 0) {  // no view: full tree (k_gradient, hard list)
+            if (lane == 0) g.fallback[px - 1u - atomicAdd(&counters[kCntFallbackHard], 1u)] = p;
+            continue;
+        }
+        const IntervalRec rec = vb.iv[o.x + (uint32_t)sel];
+        const uint32_t nView = rec.viewPrim & 0xFFFFu;
+        for (uint32_t j = lane; j < nView; j += 32) {
+            const uint2 nd = vb.nodes[rec.nodeOff + j];
+            sh[w][j] = nd.x;
+            sw[w][j] = nd.y;
+        }
+        __syncwarp();
+        const F3 pc = vadd<E>(cam.pos, vscale<E>(F3{r.x, r.y, r.z}, depth));
+        const float h = smax(1e-3f, E::mul(1e-4f, depth));
+        if (lane < 6) {
+            F3 tap = pc;
+            const float s = (lane & 1) ? -h : h;
+            if (lane < 2) tap.x = E::add(pc.x, s);
+            else if (lane < 4) tap.y = E::add(pc.y, s);
+            else tap.z = E::add(pc.z, s);
+            res[w][lane] = eval_staged<FastOps>(sh[w], sw[w], nView, t.words, tap);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const F3 dv{E::sub(res[w][0], res[w][1]), E::sub(res[w][2], res[w][3]), E::sub(res[w][4], res[w][5])};
+            const F3 nn = vnormalize<E>(dv);
+            g.normal[3 * p + 0] = nn.x;
+            g.normal[3 * p + 1] = nn.y;
+            g.normal[3 * p + 2] = nn.z;
+        }
+        __syncwarp();
     }
 }
 
@@ -637,8 +718,10 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
 
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
-                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps) {
+                    uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
+                    const ViewBufs* vb) {
     cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
+    cudaMemsetAsync(counters + kCntFallbackHard, 0, sizeof(uint32_t), st);
     dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
     k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
     const size_t bytes = (size_t)t.nFrontier * 6 * sizeof(float) + (size_t)t.nUpper * sizeof(uint32_t);
@@ -653,10 +736,14 @@ void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& ca
     // one CTA per queued pixel: as many threads as frontier subtrees (phase 1
     // is one subtree per thread), at least 6 warps for the min-chain phase
     const uint32_t threads = std::min<uint32_t>(1024u, std::max<uint32_t>(256u, (t.nFrontier + 31u) & ~31u));
-    if (exact)
-        k_gradient<ExactOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
-    else
-        k_gradient<FastOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem);
+    if (exact) {
+        k_gradient<ExactOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem, 0u);
+    } else if (vb) {
+        k_gradient_view<<<smCount * 2, kGradViewWarps * 32, 0, st>>>(t, cam, fb, *vb, g, counters, stats);
+        k_gradient<FastOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem, 1u);
+    } else {
+        k_gradient<FastOps><<<scratchWarps, threads, smem, st>>>(t, cam, fb, g, counters, stats, scratch, useSmem, 0u);
+    }
 }
 
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,

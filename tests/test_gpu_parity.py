@@ -123,6 +123,45 @@ def test_fast_mode_within_tolerance(rd, name):
     assert (ge.tileError == gf.tileError).all()
 
 
+def _fallback_pixels(hit: np.ndarray, w: int, h: int) -> np.ndarray:
+    """Hit pixels whose depth-differential normal is undefined -- no hit
+    neighbour left/right or up/down (tracer.cpp:296-350) -- i.e. the pixels
+    that take the 6-tap gradient fallback."""
+    hm = hit.reshape(h, w).astype(bool)
+    p = np.pad(hm, 1)
+    lr = p[1:-1, :-2] | p[1:-1, 2:]
+    ud = p[:-2, 1:-1] | p[2:, 1:-1]
+    return (hm & ~(lr & ud)).reshape(-1)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5", "C2"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fast_gradient_fallback_matches_full_tree(rd, name, mode):
+    """FMA path: the gradient (the fallback of mode 0, every hit pixel in
+    central mode 1) evaluates the pruned view of the interval the ray hit in;
+    the exact path evaluates the full tree like the reference.  Where both
+    modes hit the same surface point the normals agree."""
+    cfg = RenderConfig()
+    cfg.normalsMode = mode
+    s = Scene.build(name)
+    rd.upload(s)
+    cam = s.device_camera
+    rd.render_frame(cam, cfg, exact=True, graph=False)
+    ge = rd.download_gbuffer()
+    rd.render_frame(cam, cfg, exact=False, graph=False)
+    gf = rd.download_gbuffer()
+    both = (ge.hit == 1) & (gf.hit == 1)
+    sel = both if mode == 1 else both & _fallback_pixels(ge.hit, s.width, s.height) & _fallback_pixels(
+        gf.hit, s.width, s.height)
+    if mode == 0 and sel.sum() < 10:
+        pytest.skip("too few fallback pixels in this scene (mode 1 covers the gradient)")
+    dt = np.abs(ge.depth[sel].astype(np.float64) - gf.depth[sel])
+    near = dt <= 1e-4 * ge.depth[sel]  # same surface point (grazing outliers excluded)
+    dots = (ge.normal[sel][near] * gf.normal[sel][near]).sum(1)
+    assert near.mean() >= 0.9
+    assert (dots >= 0.999).mean() >= 0.995, (near.mean(), np.sort(dots)[:5])
+
+
 GOLDEN_FILES = sorted(glob.glob(os.path.join(GOLDEN, "scene_*.npz")))
 
 
