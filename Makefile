@@ -36,7 +36,7 @@ API_HDRS := $(wildcard include/blobtree/*.hpp) include/bt_cuda.h
 
 .PHONY: all lib oracle all-ref clean
 all: lib oracle
-lib: $(LIB)/libblobtree_b200.so $(LIB)/libbt_scenes.so
+lib: $(LIB)/libblobtree_b200.so $(LIB)/libbt_scenes.so $(LIB)/blobtree_render
 
 $(OBJ)/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	@mkdir -p $(dir $@)
@@ -53,6 +53,10 @@ $(LIB)/libblobtree_b200.so: $(CU_OBJS) $(CPP_OBJS)
 $(LIB)/libbt_scenes.so: $(CSRC)/scenes/scenes.cpp $(CSRC)/scenes/scenes.hpp $(LIB)/libblobtree_b200.so
 	$(CXX) $(CXXFLAGS) -shared -DSCENE_PREFIX=sc_ -DSCENE_PRODUCT $(CSRC)/scenes/scenes.cpp -o $@ \
 	    -L$(LIB) -lblobtree_b200 -Wl,-rpath,'$$ORIGIN'
+
+# the reference's specified command-line harness (SPEC.md cli-harness)
+$(LIB)/blobtree_render: $(CSRC)/tools/blobtree_render.cpp $(API_HDRS) $(LIB)/libblobtree_b200.so
+	$(CXX) $(CXXFLAGS) $(CSRC)/tools/blobtree_render.cpp -o $@ -L$(LIB) -lblobtree_b200 -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle port
