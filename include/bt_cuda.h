@@ -156,6 +156,12 @@ BT_API int bt_tree_upload(bt_ctx* ctx, const float* data, uint32_t nwords,
  * after host validation): entry i rewrites count[i] floats at
  * data[4*(words[i]+1)] from params[i*stride ...].  Host buffers (H2D inside)
  * or device buffers (_device variant, for the resident fast path). */
+/* compute_fast_indices (linear_tree.cpp:150-168) on the uploaded tree, in
+ * place on the device: every blob's ancestor becomes its fast target.  A
+ * tree uploaded with parent ancestors (compile() only) ends up bit-identical
+ * to one compiled with compute_fast_indices on the host; pointer jumping,
+ * O(n log n) work instead of O(n x chain length).  bt_tree_download reads it. */
+BT_API int bt_tree_fast_indices(bt_ctx* ctx);
 BT_API int bt_params_update(bt_ctx* ctx, const uint32_t* words, const float* params,
                             const uint32_t* counts, uint32_t n, uint32_t stride);
 BT_API int bt_params_update_device(bt_ctx* ctx, const uint32_t* d_words, const float* d_params,

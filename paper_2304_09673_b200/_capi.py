@@ -78,6 +78,7 @@ PROTOTYPES = {
     "bt_params_update": [vp, vp, vp, vp, u32, u32],
     "bt_params_update_device": [vp, vp, vp, vp, u32, u32],
     "bt_tree_download": [vp, vp, u32],
+    "bt_tree_fast_indices": [vp],
     "bt_roi": [vp, vp, u32],
     "bt_roi_upload": [vp, vp, u32],
     "bt_voi_build": [vp, f32],

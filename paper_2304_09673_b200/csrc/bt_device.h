@@ -125,6 +125,11 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
                     int smCount);
 void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
 
+// ---- launchers (k_tree.cu) -------------------------------------------
+// compute_fast_indices on the device words (scratch: 4 n int32)
+void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWord, const int32_t* parentOrd,
+                         uint32_t n, int32_t* scratch);
+
 // ---- launchers (k_views.cu) -------------------------------------------
 // build=false: count pass + scan (the host may then read the totals and grow
 // the record buffers); build=true: write the interval/view records.

@@ -86,7 +86,7 @@ struct bt_ctx {
     DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram;
     DevBuf<uint2> frontier;
     uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0, upperIsMinChain = 0;
-    DevBuf<int32_t> compactAnc;
+    DevBuf<int32_t> compactAnc, parentOrd, fastScratch;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
     uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
@@ -545,6 +545,8 @@ int bt_ctx_destroy(bt_ctx* c) {
         b->release();
     c->words.release();
     c->compactAnc.release();
+    c->parentOrd.release();
+    c->fastScratch.release();
     c->roi.release();
     c->vois.release();
     c->pParams.release();
@@ -706,6 +708,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(c->primOrd.reserve(nprims));
     BT_CUDA(c->nodeWord.reserve(nnodes));
     BT_CUDA(c->compactAnc.reserve(nnodes));
+    BT_CUDA(c->parentOrd.reserve(nnodes));
     BT_CUDA(c->fullProgram.reserve(nnodes));
     BT_CUDA(c->roi.reserve(nnodes));
     BT_CUDA(c->frontier.reserve(frontier.size()));
@@ -717,6 +720,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->primOrd.ptr, primOrd.data(), nprims * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->nodeWord.ptr, nodeWord.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->compactAnc.ptr, compactAnc.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemcpyAsync(c->parentOrd.ptr, parentOrd.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->fullProgram.ptr, program.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->frontier.ptr, frontier.data(), frontier.size() * sizeof(uint2), cudaMemcpyHostToDevice,
                             c->stream));
@@ -743,6 +747,14 @@ int bt_tree_download(bt_ctx* c, float* data, uint32_t nwords) {
     if (nwords > c->nwords) return fail(BT_EINVAL, "nwords exceeds the uploaded tree");
     BT_CUDA(cudaMemcpyAsync(data, c->words.ptr, (size_t)nwords * 16, cudaMemcpyDeviceToHost, c->stream));
     BT_CUDA(cudaStreamSynchronize(c->stream));
+    return BT_OK;
+}
+
+int bt_tree_fast_indices(bt_ctx* c) {
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    BT_CUDA(c->fastScratch.reserve((size_t)c->nnodes * 4));
+    launch_fast_indices(c->stream, c->words.ptr, c->nodeWord.ptr, c->parentOrd.ptr, c->nnodes, c->fastScratch.ptr);
+    BT_CUDA(cudaGetLastError());
     return BT_OK;
 }
 

@@ -44,9 +44,17 @@ for name in sys.argv[1:] or ["C3", "C5", "C2", "C1"]:
     np.add.at(span, tid, (fr["zExit"] - fr["zEntry"]).astype(np.float64))
     spanmax = np.zeros(len(cnt))
     np.maximum.at(spanmax, tid, (fr["zExit"] - fr["zEntry"]).astype(np.float64))
+    # view-z extents (linear in depth, like the march steps)
+    cam14 = cam
+    inv_near, idr = cam.invNear, cam.invDepthRange
+    vz = lambda z: 1.0 / (inv_near - z / idr)  # noqa: E731  (view_z_from_ndc)
+    vspan = np.zeros(len(cnt))
+    np.add.at(vspan, tid, (vz(fr["zExit"].astype(np.float64)) - vz(fr["zEntry"].astype(np.float64))))
+    vmax = np.zeros(len(cnt))
+    np.maximum.at(vmax, tid, (vz(fr["zExit"].astype(np.float64)) - vz(fr["zEntry"].astype(np.float64))))
     res = {"raster": march_ms(rd, cam, c)}
-    for key, cost in (("truth:max", t.max(1)), ("cnt", cnt), ("span", span), ("spanmax", spanmax),
-                      ("cnt*spanmax", cnt * spanmax)):
+    for key, cost in (("truth:max", t.max(1)), ("cnt", cnt), ("span", span), ("vspan", vspan), ("vmax", vmax),
+                      ("cnt+4span", 4 * cnt + 16 * span), ("vspan+cnt", vspan / max(vspan.mean(), 1e-9) + cnt / max(cnt.mean(), 1e-9))):
         order = np.argsort(-cost, kind="stable").astype(np.uint32)
         capi.check(rd.lib.bt_set_tile_order(rd.ctx, order.ctypes.data_as(C.c_void_p), len(order)), "order")
         res[key] = march_ms(rd, cam, c)

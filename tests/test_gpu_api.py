@@ -263,3 +263,34 @@ def test_march_schedule_never_changes_results(rd):
         assert st == bst
         for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
             assert getattr(g, plane).tobytes() == getattr(base, plane).tobytes(), plane
+
+
+@pytest.mark.parametrize("name", ["C3", "C5", "comb_error", "random:24", "csg", "gen:cells:40:mixed:smooth"])
+def test_device_fast_indices_equal_host(rd, name):
+    """GPU tree preprocessing: a tree uploaded with plain
+    parent ancestors, then bt_tree_fast_indices on the device, is bit-identical
+    to the host compute_fast_indices result -- and renders identically."""
+    seed = 7 if name.startswith("gen") else 0
+    s = Scene.build(name, seed)
+    fast = s.data.copy()
+    data = s.data.copy()
+    blobs = data.view(np.uint32)
+    for n in s.nodes:  # blob ancestor := parent word (the root keeps the sentinel)
+        w = int(n["word"]) * 4
+        anc = int(n["parentWord"]) & 0x7FFFFF
+        blobs[w] = (int(blobs[w]) & ~0x7FFFFF) | anc
+    assert data.tobytes() != fast.tobytes() or name == "csg"
+    s.data = data  # upload the parent-pointer tree
+    rd.upload(s)
+    s.data = fast
+    assert rd.lib.bt_tree_fast_indices(rd.ctx) == 0
+    got = rd.tree_words()
+    assert got.view(np.uint32).tobytes() == fast.view(np.uint32).tobytes()
+    cfg = RenderConfig()
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    a = rd.download_gbuffer()
+    rd.upload(s)
+    rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+    b = rd.download_gbuffer()
+    for plane in ("hit", "depth", "evalCount", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert getattr(a, plane).tobytes() == getattr(b, plane).tobytes(), plane
