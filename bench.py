@@ -207,16 +207,45 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes, tile_row_ranges
     planes = {}
 
+    # Multi-GPU exchange.  Preferred: the fused gather -- rank 0 exports its
+    # G-buffer planes (CUDA IPC), the other ranks import them and their marches
+    # write their rows straight into rank 0's G-buffer over NVLink while they
+    # run; a one-element all-reduce on the stream then orders rank 0's normals
+    # after every rank's march.  Fallback: NCCL gather of the rows.
+    fused = False
+    if world > 1:
+        import ctypes as _C
+        import torch.distributed as dist
+        rd.render_frame(cam, cfg, exact=exact, graph=False, tile0=tile0, tile1=tile1, normals=False)
+        torch.cuda.synchronize(dev)
+        ok = 1
+        h = capi.bt_ipc_handles()
+        if rank == 0 and lib.bt_gbuffer_export(rd.ctx, _C.byref(h)) != 0:
+            ok = 0
+        obj = [bytes(h), ok]
+        dist.broadcast_object_list(obj, src=0)
+        if obj[1] and rank != 0:
+            _C.memmove(_C.addressof(h), obj[0], _C.sizeof(h))
+            ok = 1 if lib.bt_gbuffer_import(rd.ctx, _C.byref(h)) == 0 else 0
+        flag = torch.tensor([ok if obj[1] else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        fused = bool(flag.item())
+        if not fused and rank != 0:
+            lib.bt_gbuffer_import_release(rd.ctx)
+        done = torch.zeros(1, dtype=torch.int32, device=dev)
+
     def step(f):
         rd.update_params_device(d_words[f].data_ptr(), d_params[f].data_ptr(), d_counts[f].data_ptr(), nprim)
         rd.render_frame(cam, cfg, exact=exact, graph=True, tile0=tile0, tile1=tile1, normals=(world == 1))
         if world > 1:
-            # the only exchange: this rank's rows of hit/depth/evalCount -> rank 0,
-            # then normals over the whole image on rank 0 (they need neighbour rows)
-            if not planes:
-                planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
-            gather_rows(planes, rows, rank, world, W, H)
-            if rank == 0:
+            if fused:
+                dist.all_reduce(done)  # stream-ordered: every rank's march has written its rows
+            else:
+                # this rank's rows of hit/depth/evalCount -> rank 0 (NCCL)
+                if not planes:
+                    planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
+                gather_rows(planes, rows, rank, world, W, H)
+            if rank == 0:  # normals over the whole image (they need neighbour rows)
                 rd.compute_normals(cam, cfg.normalsMode, exact)
 
     for f in range(args.warmup):
@@ -262,7 +291,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                    "resolution": f"{W}x{H}", "rays_per_frame": W * H,
                    "field_eval": "ieee-exact" if exact else "fma-contracted (tolerance path)",
                    "l2": "flushed between timed frames (256 MiB device write, untimed)",
-                   "parallelism": f"tile rows over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "parallelism": (f"tile rows over {world} GPU(s), "
+                                   f"{'fused gather (IPC peer writes)' if fused else 'NCCL gather'}")
+                                  if world > 1 else "1 GPU",
                    "graph": f"{kernels.value} kernels / {nodes.value} nodes per frame"},
         "gpu_launches": launches,
         "clocks": {k: clock[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
@@ -486,11 +517,18 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if os.environ.get("BT_BENCH_SHARE_GPU") == "1":
+        # test mode: every rank on GPU 0, gloo -- exercises the multi-rank code
+        # path (fused gather via IPC included) on a one-GPU box; not a measurement
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("BT_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

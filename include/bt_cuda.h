@@ -223,6 +223,22 @@ BT_API int bt_gbuffer_download_async(bt_ctx* ctx, uint8_t* hit, float* depth, fl
                                      uint32_t* evalCount, uint32_t* tileMaxOverlap,
                                      uint32_t* tileCacheBytes, uint8_t* tileError);
 BT_API int bt_download_wait(bt_ctx* ctx);
+
+/* Fused gather over peer memory (multi-GPU).  The root rank
+ * exports its G-buffer planes as CUDA IPC handles; every other rank imports
+ * them, after which its traces write their tiles' pixels (hit, depth,
+ * evalCount) and tile planes straight into the root's G-buffer over
+ * NVLink, while the march runs -- no separate gather.  The image size must
+ * match; the root must not resize its image while handles are imported.
+ * After the ranks' streams are done (a host barrier), the root computes the
+ * normals of the assembled frame. */
+typedef struct bt_ipc_handles {
+    unsigned char plane[6][64]; /* hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError */
+    int32_t width, height;
+} bt_ipc_handles;
+BT_API int bt_gbuffer_export(bt_ctx* ctx, bt_ipc_handles* out);
+BT_API int bt_gbuffer_import(bt_ctx* ctx, const bt_ipc_handles* in);
+BT_API int bt_gbuffer_import_release(bt_ctx* ctx);
 /* March scheduling.  The persistent march kernel ends with its slowest tile,
  * so by default (mode 1) the tiles are queued longest-first by a cost proxy
  * computed with the interval count (fragments and their depth extent;

@@ -48,6 +48,10 @@ class bt_fragment(C.Structure):
     _fields_ = [("primitiveWord", C.c_uint32), ("zEntry", C.c_float), ("zExit", C.c_float)]
 
 
+class bt_ipc_handles(C.Structure):
+    _fields_ = [("plane", (C.c_ubyte * 64) * 6), ("width", C.c_int32), ("height", C.c_int32)]
+
+
 class bt_stats(C.Structure):
     _fields_ = [("fieldEvals", C.c_uint64), ("retainedNodeVisits", C.c_uint64),
                 ("primitiveEvals", C.c_uint64), ("treeNodeCount", C.c_uint64),
@@ -96,6 +100,9 @@ PROTOTYPES = {
     "bt_gbuffer_download_async": [vp, vp, vp, vp, vp, vp, vp, vp],
     "bt_download_wait": [vp],
     "bt_set_tile_order": [vp, vp, u32],
+    "bt_gbuffer_export": [vp, vp],
+    "bt_gbuffer_import": [vp, vp],
+    "bt_gbuffer_import_release": [vp],
     "bt_set_scheduling": [vp, C.c_int],
     "bt_gbuffer_device": [vp, P(bt_gbuffer_view)],
     "bt_gbuffer_upload": [vp, P(bt_camera), vp, vp],

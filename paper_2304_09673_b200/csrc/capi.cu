@@ -122,6 +122,14 @@ struct bt_ctx {
     bool dlPending[2] = {false, false};
     int dlSlot = 0;
 
+    // fused gather (bt_gbuffer_import): the march writes its pixels and tile
+    // planes straight into another context's G-buffer (CUDA IPC, peer memory)
+    struct Remote {
+        bool on = false;
+        void* p[6] = {};  // hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError
+        int width = 0, height = 0;
+    } remote;
+
     DevBuf<uint64_t> stats;
     // compiled intervals / pruned views of stage (c) (k_views.cu)
     DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
@@ -228,6 +236,31 @@ GBuf gbuf(const bt_ctx* c) {
     g.tilesX = c->tilesX;
     g.tilesY = c->tilesY;
     return g;
+}
+
+// G-buffer targets of the march: the context's own planes, or the imported
+// planes of another context (fused gather) when the image size matches.
+GBuf trace_gbuf(const bt_ctx* c) {
+    GBuf g = gbuf(c);
+    if (c->remote.on && c->remote.width == c->width && c->remote.height == c->height) {
+        g.hit = static_cast<uint8_t*>(c->remote.p[0]);
+        g.depth = static_cast<float*>(c->remote.p[1]);
+        g.evalCount = static_cast<uint32_t*>(c->remote.p[2]);
+        g.tileMaxOverlap = static_cast<uint32_t*>(c->remote.p[3]);
+        g.tileCacheBytes = static_cast<uint32_t*>(c->remote.p[4]);
+        g.tileError = static_cast<uint8_t*>(c->remote.p[5]);
+    }
+    return g;
+}
+
+void release_remote(bt_ctx* c) {
+    if (!c->remote.on) return;
+    for (void*& q : c->remote.p) {
+        if (q) cudaIpcCloseMemHandle(q);
+        q = nullptr;
+    }
+    c->remote.on = false;
+    c->bufEpoch++;
 }
 
 Cam to_cam(const bt_camera& k) {
@@ -427,7 +460,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
     if (c->schedMode == 1)  // longest-first march units from the count pass's cost proxy
-        launch_tile_order(c->stream, view_bufs(c), gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
+        launch_tile_order(c->stream, view_bufs(c), trace_gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
                           trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
     if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
     if (checked) {
@@ -453,7 +486,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         vbm.order = c->tileOrder.ptr;
         vbm.unitCount = c->hostUnits.ptr;
     }
-    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, gbuf(c), c->stats.ptr, tile0, tile1,
+    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, trace_gbuf(c), c->stats.ptr, tile0, tile1,
                  c->smCount, c->tileQueue.ptr);
     if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
@@ -575,6 +608,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->orderHist.release();
     c->tileQueue.release();
     for (auto& e : c->ev) cudaEventDestroy(e);
+    release_remote(c);
     if (c->copyStream) {
         cudaStreamSynchronize(c->copyStream);
         cudaStreamDestroy(c->copyStream);
@@ -1158,6 +1192,49 @@ int bt_set_scheduling(bt_ctx* c, int mode) {
     if (mode != 0 && mode != 1) return fail(BT_EINVAL, "scheduling mode must be 0 (raster) or 1 (longest-first)");
     c->schedMode = mode;
     c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_gbuffer_export(bt_ctx* c, bt_ipc_handles* out) {
+    if (!c || !out) return fail(BT_EINVAL, "null argument");
+    if (!c->hit.ptr) return fail(BT_ESTATE, "no G-buffer allocated (render a frame first)");
+    void* planes[6] = {c->hit.ptr, c->depth.ptr, c->evalCount.ptr, c->tileMaxOverlap.ptr, c->tileCacheBytes.ptr,
+                       c->tileError.ptr};
+    for (int i = 0; i < 6; ++i) {
+        cudaIpcMemHandle_t h;
+        BT_CUDA(cudaIpcGetMemHandle(&h, planes[i]));
+        static_assert(sizeof(h) == sizeof(out->plane[0]), "IPC handle size");
+        std::memcpy(out->plane[i], &h, sizeof(h));
+    }
+    out->width = c->width;
+    out->height = c->height;
+    return BT_OK;
+}
+
+int bt_gbuffer_import(bt_ctx* c, const bt_ipc_handles* in) {
+    if (!c || !in) return fail(BT_EINVAL, "null argument");
+    release_remote(c);
+    for (int i = 0; i < 6; ++i) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, in->plane[i], sizeof(h));
+        void* q = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            release_remote(c);
+            return fail(BT_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        c->remote.p[i] = q;
+    }
+    c->remote.on = true;
+    c->remote.width = in->width;
+    c->remote.height = in->height;
+    c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_gbuffer_import_release(bt_ctx* c) {
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    release_remote(c);
     return BT_OK;
 }
 
