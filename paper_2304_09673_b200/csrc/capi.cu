@@ -116,7 +116,7 @@ struct bt_ctx {
     bool haveGbuffer = false;
 
     // streaming download (bt_gbuffer_download_async): two device snapshot slots
-    cudaStream_t copyStream = nullptr;
+    cudaStream_t copyStream = nullptr, copyStream2 = nullptr;  // one per snapshot slot
     DevBuf<uint8_t> snap[2];
     cudaEvent_t evSnap[2] = {}, evCopied[2] = {};
     bool dlPending[2] = {false, false};
@@ -611,7 +611,9 @@ int bt_ctx_destroy(bt_ctx* c) {
     release_remote(c);
     if (c->copyStream) {
         cudaStreamSynchronize(c->copyStream);
+        cudaStreamSynchronize(c->copyStream2);
         cudaStreamDestroy(c->copyStream);
+        cudaStreamDestroy(c->copyStream2);
         for (int i = 0; i < 2; ++i) {
             cudaEventDestroy(c->evSnap[i]);
             cudaEventDestroy(c->evCopied[i]);
@@ -627,6 +629,7 @@ int bt_sync(bt_ctx* c) {
     if (!c) return fail(BT_EINVAL, "ctx is null");
     BT_CUDA(cudaStreamSynchronize(c->stream));
     if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
+    if (c->copyStream2) BT_CUDA(cudaStreamSynchronize(c->copyStream2));
     BT_CUDA(cudaGetLastError());
     return BT_OK;
 }
@@ -1146,6 +1149,7 @@ int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* norm
     }
     if (!c->copyStream) {
         BT_CUDA(cudaStreamCreateWithFlags(&c->copyStream, cudaStreamNonBlocking));
+        BT_CUDA(cudaStreamCreateWithFlags(&c->copyStream2, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
             BT_CUDA(cudaEventCreateWithFlags(&c->evSnap[i], cudaEventDisableTiming));
             BT_CUDA(cudaEventCreateWithFlags(&c->evCopied[i], cudaEventDisableTiming));
@@ -1153,19 +1157,20 @@ int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* norm
     }
     const int slot = c->dlSlot;
     c->dlSlot ^= 1;
+    cudaStream_t cs = slot ? c->copyStream2 : c->copyStream;  // consecutive frames' copies may overlap
     if (c->dlPending[slot]) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evCopied[slot], 0));  // slot free again
     if (c->snap[slot].cap < total) {
-        BT_CUDA(cudaStreamSynchronize(c->copyStream));
+        BT_CUDA(cudaStreamSynchronize(cs));
         BT_CUDA(c->snap[slot].reserve(total));
     }
     uint8_t* base = c->snap[slot].ptr;
     for (int i = 0; i < 7; ++i)
         if (dst[i]) BT_CUDA(cudaMemcpyAsync(base + off[i], src[i], sz[i], cudaMemcpyDeviceToDevice, c->stream));
     BT_CUDA(cudaEventRecord(c->evSnap[slot], c->stream));
-    BT_CUDA(cudaStreamWaitEvent(c->copyStream, c->evSnap[slot], 0));
+    BT_CUDA(cudaStreamWaitEvent(cs, c->evSnap[slot], 0));
     for (int i = 0; i < 7; ++i)
-        if (dst[i]) BT_CUDA(cudaMemcpyAsync(dst[i], base + off[i], sz[i], cudaMemcpyDeviceToHost, c->copyStream));
-    BT_CUDA(cudaEventRecord(c->evCopied[slot], c->copyStream));
+        if (dst[i]) BT_CUDA(cudaMemcpyAsync(dst[i], base + off[i], sz[i], cudaMemcpyDeviceToHost, cs));
+    BT_CUDA(cudaEventRecord(c->evCopied[slot], cs));
     c->dlPending[slot] = true;
     return BT_OK;
 }
@@ -1241,6 +1246,7 @@ int bt_gbuffer_import_release(bt_ctx* c) {
 int bt_download_wait(bt_ctx* c) {
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
+    if (c->copyStream2) BT_CUDA(cudaStreamSynchronize(c->copyStream2));
     BT_CUDA(cudaGetLastError());
     return BT_OK;
 }
