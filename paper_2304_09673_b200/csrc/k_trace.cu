@@ -69,6 +69,9 @@ struct MarchSmem {
     uint32_t evals[64];
     uint8_t hit[64];
     uint8_t pend[64];             // rays still to march in this interval, in order
+    // per-tile accounting, kept here rather than in registers live across the march
+    uint32_t accFe[32], accFl[32], accRnv[32], accPe[32];
+    uint32_t tileMaxOv, tileCache, tileErr, steps;
 };
 
 // Per-block work accounting, flushed to the device statistics once per CTA.
@@ -126,8 +129,19 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
     }
 }
 
+// Rays of this unit that are inside the image: bit l of word j = ray l + 32j.
+__device__ __forceinline__ void unit_rays(const GBuf& g, int tx, int ty, uint32_t mine, uint32_t& v0, uint32_t& v1) {
+    const int lane = threadIdx.x & 31;
+    const int px = tx * kTile + (lane & 7);
+    const int py0 = ty * kTile + (lane >> 3), py1 = py0 + 4;
+    v0 = __ballot_sync(kFull, px < g.width && py0 < g.height) & mine;
+    v1 = __ballot_sync(kFull, px < g.width && py1 < g.height) & mine;
+}
+
 // One 8x8 tile: walk its compiled intervals until all 64 rays have hit
-// (tracer.cpp:165-230), then write its pixels and tile planes.
+// (tracer.cpp:165-230), then write its pixels and tile planes.  The tile's
+// bookkeeping lives in the warp's shared memory, not in registers that would
+// stay live across the march loop.
 template <class O>
 __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
                                            const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
@@ -138,25 +152,16 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
     const bool half = (unit & kUnitSplit) != 0u;
     const uint32_t mine = !half ? kFull : ((unit & kUnitPart1) ? 0xAAAAAAAAu : 0x55555555u);
     const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
-    int px[2], py[2];
-    bool valid[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int li = lane + 32 * j;
-        px[j] = tx * kTile + (li & 7);
-        py[j] = ty * kTile + (li >> 3);
-        valid[j] = px[j] < g.width && py[j] < g.height;
-        s.hit[li] = 0;
-        s.evals[li] = 0;
-    }
-    uint32_t found0 = ~(__ballot_sync(kFull, valid[0]) & mine), found1 = ~(__ballot_sync(kFull, valid[1]) & mine);
-    valid[0] = valid[0] && ((mine >> lane) & 1u);
-    valid[1] = valid[1] && ((mine >> lane) & 1u);
-    uint32_t tileMaxOv = 0, tileCache = 0, tileErr = 0;
-    uint32_t fe = 0, rnv = 0, pe = 0, fl = 0, steps = 0;
+    s.hit[lane] = 0;
+    s.hit[lane + 32] = 0;
+    s.evals[lane] = 0;
+    s.evals[lane + 32] = 0;
+    s.accFe[lane] = s.accFl[lane] = s.accRnv[lane] = s.accPe[lane] = 0;
+    if (lane == 0) s.tileMaxOv = s.tileCache = s.tileErr = s.steps = 0;
+    __syncwarp();
     const uint2 c = vb.count[tile];
     if (c.x != 0u && vb.counters[1] != 0u) {
-        tileErr = 1;  // interval records overflowed in a graph replay (flagged to the host)
+        if (lane == 0) s.tileErr = 1;  // interval records overflowed in a graph replay (flagged to the host)
     } else if (c.x != 0u) {
         const uint2 o = view_offset(vb, tile);
 #pragma unroll
@@ -166,24 +171,28 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             s.rays[lane + 32 * j] = r;
         }
         for (uint32_t k = 0; k < c.x; ++k) {
+            uint32_t v0, v1;
+            unit_rays(g, tx, ty, mine, v0, v1);
+            const uint32_t found0 = ~v0 | __ballot_sync(kFull, s.hit[lane] != 0);
+            const uint32_t found1 = ~v1 | __ballot_sync(kFull, s.hit[lane + 32] != 0);
             if ((found0 & found1) == kFull) break;
             const uint4* rp = reinterpret_cast<const uint4*>(vb.iv + o.x + k);
             const uint4 ra = rp[0], rb = rp[1];
             const uint32_t flags = rb.x >> 8;
-            tileMaxOv = max(tileMaxOv, rb.x & 0xFFu);
+            if (lane == 0) s.tileMaxOv = max(s.tileMaxOv, rb.x & 0xFFu);
             if (flags & kIvErr) {
-                tileErr = 1;
+                if (lane == 0) s.tileErr = 1;
                 break;
             }
-            tileCache = max(tileCache, rb.y);
+            if (lane == 0) s.tileCache = max(s.tileCache, rb.y);
             if (!(flags & kIvRootUsed)) continue;
             const float zb = __uint_as_float(ra.x), ze = __uint_as_float(ra.y);
             if (ze <= zb) continue;
             if (flags & kIvDepthErr) {  // eval_pruned would throw on first use
-                tileErr = 1;
+                if (lane == 0) s.tileErr = 1;
                 break;
             }
-            const uint32_t nView = ra.w & 0xFFFFu, nPrim = ra.w >> 16;
+            const uint32_t nView = ra.w & 0xFFFFu;
             // fast path: evaluation-ready parameter blocks in shared memory when
             // the view fits (the common case); otherwise raw parameters
             const bool fits = rb.w <= kMarchBlocks;
@@ -200,30 +209,34 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             if ((p1 >> lane) & 1u) s.pend[c0 + __popc(p1 & lt)] = (uint8_t)(lane + 32);
             __syncwarp();
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
-            uint32_t ife = 0, ifl = 0;
-            march_interval<O>(t, cam, tp, s, fits, nView, nPend, vz0, vz1, lt, ife, ifl, steps, rb.z);
-            fe += ife;
-            fl += ifl;
-            rnv += ife * nView;
-            pe += ife * nPrim;
+            uint32_t ife = 0, ifl = 0, isteps = 0;
+            march_interval<O>(t, cam, tp, s, fits, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+            s.accFe[lane] += ife;
+            s.accFl[lane] += ifl;
+            s.accRnv[lane] += ife * nView;
+            s.accPe[lane] += ife * (ra.w >> 16);
+            if (lane == 0) s.steps += isteps;
             __syncwarp();
-            found0 |= __ballot_sync(kFull, s.hit[lane] != 0);
-            found1 |= __ballot_sync(kFull, s.hit[lane + 32] != 0);
         }
     }
     __syncwarp();
+    uint32_t v0, v1;
+    unit_rays(g, tx, ty, mine, v0, v1);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        if (!valid[j]) continue;
+        if (!(((j ? v1 : v0) >> lane) & 1u)) continue;
         const int li = lane + 32 * j;
-        const size_t p = (size_t)py[j] * g.width + px[j];
+        const size_t p = (size_t)(ty * kTile + (li >> 3)) * g.width + tx * kTile + (li & 7);
         const bool h = s.hit[li] != 0;
         g.hit[p] = h ? 1 : 0;
         g.depth[p] = h ? s.depth[li] : 0.0f;
         g.evalCount[p] = s.evals[li];
     }
-    const uint64_t sfe = warp_sum_u64(fe), srnv = warp_sum_u64(rnv), spe = warp_sum_u64(pe), sfl = warp_sum_u64(fl);
+    const uint64_t sfe = warp_sum_u64(s.accFe[lane]), srnv = warp_sum_u64(s.accRnv[lane]);
+    const uint64_t spe = warp_sum_u64(s.accPe[lane]), sfl = warp_sum_u64(s.accFl[lane]);
     if (lane == 0) {
+        const uint32_t tileMaxOv = s.tileMaxOv, tileCache = s.tileCache;
+        uint32_t tileErr = s.tileErr;
         if (!half) {
             g.tileMaxOverlap[tile] = tileMaxOv;
             g.tileCacheBytes[tile] = tileCache;
@@ -242,7 +255,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             atomicAdd(&bs.pe, (unsigned long long)spe);
             atomicAdd(&bs.fl, (unsigned long long)sfl);
         }
-        if (steps) atomicAdd(&bs.steps, (unsigned long long)steps);
+        if (s.steps) atomicAdd(&bs.steps, (unsigned long long)s.steps);
         if (tileErr) atomicAdd(&bs.errs, 1ull);
         if (tileMaxOv) atomicMax(&bs.maxOv, tileMaxOv);
         if (tileCache) atomicMax(&bs.maxCache, tileCache);
