@@ -217,6 +217,8 @@ BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
     return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
 }
 
+constexpr uint32_t kNotAnOp = 0x80000000u;  // a primitive header: ends a fused primitive + operator pair
+
 // Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks in
 // this warp's shared memory), at NP points per lane.  The two top stack
 // entries live in registers (t0 = top, t1 = second): a left comb -- the
@@ -235,6 +237,18 @@ BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, c
         if (blob_is_prim(b)) {
             float v[NP];
             fast_primitive<NP>(blob_op(b), B, p, v);
+            // a primitive directly followed by an operator (every step of a
+            // left comb, the common blobtree shape): combine with the stack top
+            // in place, no push / pop
+            const uint32_t bn = i + 1 < n ? hdr[i + 1] : kNotAnOp;
+            if (sp >= 1u && !blob_is_prim(bn)) {
+                const uint32_t code = blob_op(bn);
+                const float4* Bo = prm + (bn & 0xFFFu);
+#pragma unroll
+                for (int k = 0; k < NP; ++k) t0[k] = fast_operator(code, Bo, t0[k], v[k]);
+                ++i;
+                continue;
+            }
             if (sp >= 2u) {
 #pragma unroll
                 for (int k = 0; k < NP; ++k) deep[k][sp - 2u] = t1[k];
