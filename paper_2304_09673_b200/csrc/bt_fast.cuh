@@ -231,22 +231,24 @@ BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, c
 #pragma unroll
     for (int k = 0; k < NP; ++k) t0[k] = t1[k] = 0.0f;
     uint32_t sp = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t b = hdr[i];
-        const float4* B = prm + (b & 0xFFFu);
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(prm);
+    uint32_t b = n ? hdr[0] : 0u;  // the next node's header is carried from the previous iteration
+    for (uint32_t i = 0; i < n;) {
+        const float4* B = reinterpret_cast<const float4*>(base + (b & 0xFFFFu));
+        const uint32_t bn = i + 1 < n ? hdr[i + 1] : kNotAnOp;
         if (blob_is_prim(b)) {
             float v[NP];
             fast_primitive<NP>(blob_op(b), B, p, v);
             // a primitive directly followed by an operator (every step of a
             // left comb, the common blobtree shape): combine with the stack top
             // in place, no push / pop
-            const uint32_t bn = i + 1 < n ? hdr[i + 1] : kNotAnOp;
             if (sp >= 1u && !blob_is_prim(bn)) {
                 const uint32_t code = blob_op(bn);
-                const float4* Bo = prm + (bn & 0xFFFu);
+                const float4* Bo = reinterpret_cast<const float4*>(base + (bn & 0xFFFFu));
 #pragma unroll
                 for (int k = 0; k < NP; ++k) t0[k] = fast_operator(code, Bo, t0[k], v[k]);
-                ++i;
+                i += 2;
+                b = i < n ? hdr[i] : 0u;
                 continue;
             }
             if (sp >= 2u) {
@@ -269,6 +271,8 @@ BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, c
                 for (int k = 0; k < NP; ++k) t1[k] = deep[k][sp - 2u];
             }
         }
+        ++i;
+        b = bn;
     }
 #pragma unroll
     for (int k = 0; k < NP; ++k) out[k] = t0[k];

@@ -13,7 +13,7 @@
 //   IntervalRec (32 B)  zBegin/zEnd (NDC), the view's node range, overlap,
 //                       cache bytes, flags, appendix-B flops, fast-block size
 //   ViewNode    (8 B)   hdr = isPrim(1) op(5, possibly a reserved code) |
-//                       float4 offset of the node's fast parameter block;
+//                       byte offset (bits 0-15) of the node's fast parameter block;
 //                       word = tree word of the node's parameters
 //
 // Semantics carried per record so that the march reproduces the reference
@@ -311,7 +311,7 @@ BT_DEV void view_append(ViewOut& v, uint32_t blob, uint32_t word, bool copyParam
     }
     const uint32_t floats = copyParams ? param_floats(blob) : 0u;
     if (floats > 0u && v.cacheFloats + floats <= kCacheFloats) v.cacheFloats += floats;
-    v.nodes[v.nView] = make_uint2((blob & 0xFC000000u) | v.nBlocks, word);
+    v.nodes[v.nView] = make_uint2((blob & 0xFC000000u) | (v.nBlocks << 4), word);  // byte offset of the block
     v.nBlocks += fast_block_size(blob);
     v.nView++;
     // evaluation stack depth and appendix-B flops of one evaluation

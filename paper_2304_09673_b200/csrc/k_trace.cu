@@ -63,7 +63,7 @@ template <> struct IsFast<FastOps> {
 struct MarchSmem {
     float4 blocks[kMarchBlocks];  // fast parameter blocks of the staged view
     float4 rays[64];              // dir.xyz, dot(dir, forward) of the tile's rays
-    uint32_t hdr[kViewCap];       // staged view: isPrim(1) op(5) | block offset
+    uint32_t hdr[kViewCap];       // staged view: isPrim(1) op(5) | block byte offset
     uint32_t word[kViewCap];      // exact path: tree word of each node's parameters
     float depth[64];
     uint32_t evals[64];
@@ -200,7 +200,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
                 const uint2 nd = vb.nodes[ra.z + i];
                 s.hdr[i] = nd.x;
                 s.word[i] = nd.y;
-                if (IsFast<O>::value && fits) convert_node(nd.x, t.words + nd.y + 1, s.blocks + (nd.x & 0xFFFFu));
+                if (IsFast<O>::value && fits) convert_node(nd.x, t.words + nd.y + 1, s.blocks + ((nd.x & 0xFFFFu) >> 4));
             }
             // queue of this interval: the tile's unfinished rays, in ray order
             const uint32_t p0 = ~found0, p1 = ~found1;
