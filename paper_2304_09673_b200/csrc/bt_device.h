@@ -136,6 +136,7 @@ void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWor
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
                   const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build);
 uint32_t view_scan_blocks(uint32_t tiles);
+size_t view_slab_words(uint32_t tiles);
 // longest-first march units of [tile0, tile1) from vb.tileCost (hist: 258 words of
 // scratch, [257] = unit count); tiles costing >= beta x the average work per
 // warp (at most cap of them) become two half-tile units

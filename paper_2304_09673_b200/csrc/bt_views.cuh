@@ -50,6 +50,7 @@ struct ViewBufs {
     IntervalRec* iv = nullptr;     // [ivCap]
     uint2* nodes = nullptr;        // [nodeCap] (hdr, word)
     uint32_t* counters = nullptr;  // [0] scan completion, [1] overflow flag
+    uint32_t* slab = nullptr;      // [tiles * slab stride] count-pass intervals (k_views.cu)
     const uint32_t* order = nullptr;  // optional march units in order (tile | kUnitSplit | kUnitPart1), else raster
     const uint32_t* unitCount = nullptr;  // number of entries of `order` (device)
     uint32_t* tileCost = nullptr;     // [tiles] march cost proxy 0..255 (k_view_count; scheduling)

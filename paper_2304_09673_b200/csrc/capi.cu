@@ -134,7 +134,7 @@ struct bt_ctx {
     // compiled intervals / pruned views of stage (c) (k_views.cu)
     DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
     DevBuf<IntervalRec> vIv;
-    DevBuf<uint32_t> vCounters;
+    DevBuf<uint32_t> vCounters, vSlab;
     // march scheduling: 0 raster, 1 longest-first by cost proxy (default), 2 host order
     DevBuf<uint32_t> tileOrder, tileCost, orderHist, hostUnits;
     bool viewsFrame = false;  // the G-buffer came from a whole-frame FMA-path march (its records are valid)
@@ -214,6 +214,7 @@ ViewBufs view_bufs(const bt_ctx* c) {
     v.iv = c->vIv.ptr;
     v.nodes = c->vNodes.ptr;
     v.counters = c->vCounters.ptr;
+    v.slab = c->vSlab.ptr;
     v.order = nullptr;  // chosen per trace (do_trace)
     v.tileCost = c->tileCost.ptr;
     v.ivCap = c->vIv.cap;
@@ -312,6 +313,7 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->vBlockSum.reserve(nvscan));
     BT_CUDA(c->vBlockPrefix.reserve(nvscan + 1));
     BT_CUDA(c->vCounters.reserve(2));
+    BT_CUDA(c->vSlab.reserve(view_slab_words((uint32_t)tiles)));
     BT_CUDA(c->tileCost.reserve(tiles));
     BT_CUDA(c->tileOrder.reserve(tiles * 2));
     BT_CUDA(c->orderHist.reserve(258));
@@ -602,6 +604,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     for (auto* b : {&c->vCount, &c->vLocal, &c->vBlockSum, &c->vBlockPrefix, &c->vNodes}) b->release();
     c->vIv.release();
     c->vCounters.release();
+    c->vSlab.release();
     c->tileOrder.release();
     c->tileCost.release();
     c->hostUnits.release();

@@ -28,6 +28,17 @@ __device__ __forceinline__ uint2 add2(uint2 a, uint2 b) { return make_uint2(a.x 
 
 // Warp per tile (WarpFetch): run the fetch sequence, count intervals and the
 // view-node bound; lane 0 also records the scheduling cost proxy.
+// Slab of one tile in the count pass's scratch: the intervals (zBegin, zEnd,
+// nAct) and their sorted active words, so that the fetch pass can copy
+// instead of replaying the fetch sequence.  Tiles that do not fit (more than
+// kSlabIv intervals or kSlabWords active words in total) are replayed.
+constexpr uint32_t kSlabIv = 16, kSlabWords = 96;
+constexpr uint32_t kSlabStride = 1 + 3 * kSlabIv + kSlabWords;  // u32 per tile
+constexpr uint32_t kSlabOverflow = 0xFFFFFFFFu;
+
+// Warp per tile (WarpFetch): run the fetch sequence, count intervals and the
+// view-node bound, and keep the intervals in the tile's slab; lane 0 also
+// records the scheduling cost proxy.
 __global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
                                                                 uint32_t tile0, uint32_t tile1, uint32_t tiles) {
     __shared__ WarpFetchSmem sm[kViewWarps];
@@ -38,14 +49,31 @@ __global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TracePa
     if (tile >= tile0 && tile < tile1) {
         const uint32_t off = fb.offsets[tile];
         const uint32_t cnt = fb.offsets[tile + 1] - off;
+        uint32_t* slab = vb.slab + (size_t)tile * kSlabStride;
         if (cnt) {
             WarpFetch f;
             f.init(fb.frags + off, cnt, &sm[wid], lane);
             float zb;
-            while (f.next<false>(cam, tp, zb)) {
+            uint32_t words = 0;
+            bool fits = true;
+            while (f.next<true>(cam, tp, zb)) {
+                const uint32_t n = f.n;
+                if (fits && (c.x >= kSlabIv || words + n > kSlabWords)) fits = false;
+                if (fits) {
+                    if (lane == 0) {
+                        slab[1 + 3 * c.x] = __float_as_uint(zb);
+                        slab[2 + 3 * c.x] = __float_as_uint(f.zEnd);
+                        slab[3 + 3 * c.x] = n;
+                    }
+#pragma unroll
+                    for (int sl = 0; sl < 3; ++sl)
+                        if (lane + 32u * sl < n) slab[1 + 3 * kSlabIv + words + lane + 32u * sl] = f.aW[sl];
+                    words += n;
+                }
                 c.x += 1u;
-                c.y += 2u * f.n - 1u;
+                c.y += 2u * n - 1u;
             }
+            if (lane == 0) slab[0] = fits ? c.x : kSlabOverflow;
         }
         // march cost proxy for longest-first scheduling: fragment count plus
         // the summed NDC depth extent of the tile's fragments
@@ -143,18 +171,37 @@ __global__ void __launch_bounds__(kViewWarps * 32) k_view_fetch(Cam cam, TracePa
     const uint2 c = vb.count[tile];
     if (c.x == 0 || vb.counters[1]) return;  // no intervals, or the frame overflowed (march flags it)
     const uint2 o = view_offset(vb, tile);
+    const uint32_t* slab = vb.slab + (size_t)tile * kSlabStride;
+    uint32_t nodeOff = o.y;
+    if (slab[0] != kSlabOverflow) {  // copy the count pass's intervals
+        uint32_t words = 0;
+        for (uint32_t k = 0; k < c.x; ++k) {
+            const uint32_t n = slab[3 + 3 * k];
+            uint2* act = vb.nodes + nodeOff + n - 1u;
+            for (uint32_t j = lane; j < n; j += 32) act[j].x = slab[1 + 3 * kSlabIv + words + j];
+            if (lane == 0) {
+                IntervalRec& r = vb.iv[o.x + k];
+                r.zBegin = __uint_as_float(slab[1 + 3 * k]);
+                r.zEnd = __uint_as_float(slab[2 + 3 * k]);
+                r.nodeOff = nodeOff;
+                r.actFlags = n;
+            }
+            words += n;
+            nodeOff += 2u * n - 1u;
+        }
+        return;
+    }
     const uint32_t off = fb.offsets[tile];
     const uint32_t cnt = fb.offsets[tile + 1] - off;
     WarpFetch f;
     f.init(fb.frags + off, cnt, &sm[wid], lane);
-    uint32_t nodeOff = o.y;
     float zb;
     for (uint32_t k = 0; k < c.x && f.next<true>(cam, tp, zb); ++k) {
         const uint32_t n = f.n;
         uint2* act = vb.nodes + nodeOff + n - 1u;
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
-            if (lane + 32u * s < n) act[lane + 32u * s].x = f.aW[s];
+        for (int sl = 0; sl < 3; ++sl)
+            if (lane + 32u * sl < n) act[lane + 32u * sl].x = f.aW[sl];
         if (lane == 0) {
             IntervalRec& r = vb.iv[o.x + k];
             r.zBegin = zb;
@@ -319,6 +366,8 @@ void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const Trace
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((vb.ivCap + 127) / 128, 148u * 16u);
     k_view_build<<<blocks, 128, 0, st>>>(t, vb, (tiles + kViewScanBlock - 1) / kViewScanBlock);
 }
+
+size_t view_slab_words(uint32_t tiles) { return (size_t)tiles * kSlabStride; }
 
 uint32_t view_scan_blocks(uint32_t tiles) { return (tiles + kViewScanBlock - 1) / kViewScanBlock; }
 
