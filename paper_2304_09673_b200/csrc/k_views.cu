@@ -32,7 +32,7 @@ __device__ __forceinline__ uint2 add2(uint2 a, uint2 b) { return make_uint2(a.x 
 // nAct) and their sorted active words, so that the fetch pass can copy
 // instead of replaying the fetch sequence.  Tiles that do not fit (more than
 // kSlabIv intervals or kSlabWords active words in total) are replayed.
-constexpr uint32_t kSlabIv = 16, kSlabWords = 96;
+constexpr uint32_t kSlabIv = 32, kSlabWords = 192;
 constexpr uint32_t kSlabStride = 1 + 3 * kSlabIv + kSlabWords;  // u32 per tile
 constexpr uint32_t kSlabOverflow = 0xFFFFFFFFu;
 
