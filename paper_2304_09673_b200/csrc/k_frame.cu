@@ -14,6 +14,8 @@
 // Everything on the A-buffer path is evaluated with ExactOps (no FMA, IEEE
 // div/sqrt), so (tile, word) membership and (zEntry, zExit) are bit-exact
 // with the reference's single-threaded rasterize_volumes.
+#include <algorithm>
+
 #include "bt_device.h"
 
 namespace btk {
@@ -271,17 +273,18 @@ __device__ __forceinline__ bool sb_may_touch(float4 sc, F3 apex, const Sphere& s
 __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_t nvoi, FrameBufs fb,
                                                 int tilesX, int tilesY, uint32_t tile0,
                                                 uint32_t tile1) {
+    // warp = (volume, chunk of 32 superblocks): grid.y runs over the chunks
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= nvoi) return;
     const Voi v = vois[warp];
     const Sphere bs = bounding_sphere(v);
-    const VolumeSupport sup = volume_support(v, cam.pos);
     const float vz = view_z(cam, bs.c);
     if (E::add(vz, bs.r) < cam.nearZ || E::sub(vz, bs.r) > cam.farZ) return;
+    const VolumeSupport sup = volume_support(v, cam.pos);
     const int sbX = (tilesX + kSB - 1) / kSB, sbY = (tilesY + kSB - 1) / kSB;
     const int nsb = sbX * sbY;
-    for (int base = 0; base < nsb; base += 32) {
+    for (int base = 32 * blockIdx.y; base < nsb; base += 32 * gridDim.y) {
         const int sb = base + lane;
         bool pass = false;
         if (sb < nsb) {
@@ -593,7 +596,12 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
     cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
     cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
     if (nvoi > 0) {
-        k_pairs<<<(nvoi * 32 + 255) / 256, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1);
+        const uint32_t nsb = (uint32_t)(((tilesX + kSB - 1) / kSB) * ((tilesY + kSB - 1) / kSB));
+        // enough (volume, chunk) warps to fill the GPU (~16k), no more: each
+        // warp repeats the volume's setup
+        const uint32_t chunks = std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 16384u / nvoi));
+        const dim3 grid((nvoi * 32 + 255) / 256, chunks);
+        k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1);
         k_tiles<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
         k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb);
     }
