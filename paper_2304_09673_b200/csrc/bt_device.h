@@ -125,6 +125,10 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
                     int smCount);
 void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
 
+// ---- launchers (k_util.cu) -------------------------------------------
+void launch_copy_segments(cudaStream_t st, const void* const* src, void* const* dst, const size_t* bytes, int n,
+                          int smCount);
+
 // ---- launchers (k_tree.cu) -------------------------------------------
 // compute_fast_indices on the device words (scratch: 4 n int32)
 void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWord, const int32_t* parentOrd,

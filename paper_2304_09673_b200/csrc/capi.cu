@@ -1172,8 +1172,15 @@ int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* norm
         BT_CUDA(c->snap[slot].reserve(total));
     }
     uint8_t* base = c->snap[slot].ptr;
-    for (int i = 0; i < 7; ++i)
-        if (dst[i]) BT_CUDA(cudaMemcpyAsync(base + off[i], src[i], sz[i], cudaMemcpyDeviceToDevice, c->stream));
+    {  // snapshot with an SM copy kernel: the copy engines are busy with the D2H
+        const void* s7[7];
+        void* d7[7];
+        for (int i = 0; i < 7; ++i) {
+            s7[i] = dst[i] ? src[i] : nullptr;
+            d7[i] = base + off[i];
+        }
+        launch_copy_segments(c->stream, s7, d7, sz, 7, c->smCount);
+    }
     BT_CUDA(cudaEventRecord(c->evSnap[slot], c->stream));
     // each plane goes down in two halves on two copy streams: one D2H stream
     // reaches ~33 GB/s on this PCIe link, two concurrent ones ~56 GB/s

@@ -31,7 +31,44 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
     if (s == 1234.5f) out[0] = s;  // keep the chains alive
 }
 
+// Gather-copy of up to 8 device segments (16-byte aligned) into one buffer,
+// with the SMs: the G-buffer snapshot of the streamed download, kept off the
+// copy engines that carry the D2H.
+struct CopySegs {
+    const uint4* src[8];
+    uint4* dst[8];
+    uint32_t n16[8];  // 16-byte units
+    uint32_t count;
+};
+
+__global__ void __launch_bounds__(256) k_copy_segments(CopySegs segs) {
+    for (uint32_t s = 0; s < segs.count; ++s) {
+        const uint4* __restrict__ a = segs.src[s];
+        uint4* __restrict__ b = segs.dst[s];
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < segs.n16[s]; i += gridDim.x * blockDim.x)
+            b[i] = a[i];
+    }
+}
+
 }  // namespace
+
+namespace btk {
+// src/dst pointers 16-byte aligned; bytes rounded up to 16 (the snapshot
+// slots and the G-buffer planes are cudaMalloc'd and padded)
+void launch_copy_segments(cudaStream_t st, const void* const* src, void* const* dst, const size_t* bytes, int n,
+                          int smCount) {
+    CopySegs segs{};
+    segs.count = 0;
+    for (int i = 0; i < n && segs.count < 8; ++i) {
+        if (!src[i] || !dst[i] || bytes[i] == 0) continue;
+        segs.src[segs.count] = static_cast<const uint4*>(src[i]);
+        segs.dst[segs.count] = static_cast<uint4*>(dst[i]);
+        segs.n16[segs.count] = (uint32_t)((bytes[i] + 15) / 16);
+        segs.count++;
+    }
+    if (segs.count) k_copy_segments<<<smCount * 4, 256, 0, st>>>(segs);
+}
+}  // namespace btk
 
 extern "C" BT_API int bt_fp32_peak(int device, float* tflops, float* ms_out) {
     if (cudaSetDevice(device) != cudaSuccess) return BT_ECUDA;
