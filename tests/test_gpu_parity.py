@@ -210,3 +210,49 @@ def test_abuffer_from_uploaded_reference_volumes(rd):
     off, frags = rd.rasterize_volumes(s.device_camera)
     off_ref, frags_ref = chk.rasterize(v)
     assert same(off, off_ref) and same(frags, frags_ref)
+
+
+STRESS = [
+    # name, w, h, cfg overrides: partial tiles, tiny overlap caps (view / traversal
+    # overflows -> tileError), one fragment per fetch, narrow fetch windows
+    ("C5", 203, 117, dict(maxOverlap=3, maxNewPerFetch=1, fetchWindow=0.5)),
+    ("C3", 331, 187, dict(maxOverlap=2)),
+    ("C2", 250, 141, dict(maxNewPerFetch=2, fetchWindow=1.0, normalsMode=1)),
+    ("gen:cells:60:mixed:smooth", 97, 61, dict(relax=1.0, lipschitz=1.0)),
+    ("C1", 130, 70, dict(minStep=0.02, hitEpsilon=0.01)),
+]
+
+
+@pytest.mark.parametrize("name,w,h,over", STRESS, ids=[f"{s[0]}-{s[1]}x{s[2]}" for s in STRESS])
+def test_exact_pipeline_stress_configs(rd, name, w, h, over):
+    """Odd image sizes (partial tiles) and extreme fetch / overlap settings:
+    the A-buffer, every G-buffer plane and RenderStats stay bit-identical
+    to the reference, under the default longest-first schedule with
+    half-tile units."""
+    seed = 7 if name.startswith("gen") else 0
+    cfg = RenderConfig(**over)
+    s = Scene.build(name, seed, w, h)
+    chk = Checker(s, name, seed, w, h)
+    rd.upload(s)
+    cam = s.device_camera
+    vois = rd.build_volumes_of_interest(cfg.hitEpsilon)
+    vois_ref = chk.vois(cfg.hitEpsilon)
+    assert same(vois, vois_ref)
+    off, frags = rd.rasterize_volumes(cam)
+    off_ref, frags_ref = chk.rasterize(vois_ref)
+    assert same(off, off_ref) and same(frags, frags_ref)
+    rd.reset_stats()
+    rd.render_tiles(cam, cfg, exact=True)
+    rd.compute_normals(cam, cfg.normalsMode, exact=True)
+    g = rd.download_gbuffer()
+    st = rd.stats()
+    gr, st_ref = chk.render(cfg, off_ref, frags_ref)
+    for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert same(getattr(g, plane), getattr(gr, plane)), plane
+    assert [st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals, st.treeNodeCount, st.maxOverlap,
+            st.maxCacheBytes] == st_ref
+    # the FMA path on the same stress config stays within tolerance
+    rd.render_frame(cam, cfg, exact=False, graph=False)
+    gf = rd.download_gbuffer()
+    assert (gf.hit == g.hit).mean() >= 0.999
+    assert (gf.tileError == g.tileError).all()
