@@ -372,7 +372,8 @@ def stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim, fra
     rd.profile(True)
     st = None
     flops = []
-    for f in range(frames):
+    for i in range(frames):
+        f = i % len(d_words)  # short runs (--steps 2 --warmup 1) cycle the prepared frames
         rd.update_params_device(d_words[f].data_ptr(), d_params[f].data_ptr(), d_counts[f].data_ptr(), nprim)
         rd.reset_stats()
         capi.check(lib.bt_roi(rd.ctx, None, 0), "bt_roi")

@@ -95,7 +95,8 @@ def launches(path):
             continue
         name = d["Kernel Name"].split("(")[0].replace("btk::<unnamed>::", "").replace("void ", "")
         agg[name][0] += 1
-        agg[name][1] += float(d["Metric Value"].replace(",", "")) * (1e-3 if d["Metric Unit"] == "nsecond" else 1.0)
+        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[d["Metric Unit"]]
+        agg[name][1] += float(d["Metric Value"].replace(",", "")) * scale
     return agg
 
 
