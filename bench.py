@@ -408,15 +408,25 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
     frames = [(pin(w.view(np.int32)), pin(p), pin(c.view(np.int32))) for w, p, c in host_frames]
     planes = ("hit", "depth", "normal", "evalCount", "tmo", "tcb", "terr")
 
-    def host_set():
-        return {k: torch.empty(sz, dtype=d).pin_memory() for k, sz, d in
-                (("hit", W * H, torch.uint8), ("depth", W * H, torch.float32), ("normal", W * H * 3, torch.float32),
-                 ("evalCount", W * H, torch.int32), ("tmo", tx * ty, torch.int32), ("tcb", tx * ty, torch.int32),
-                 ("terr", tx * ty, torch.uint8))}
-    outs = [host_set(), host_set()]
     lib = rd.lib
     import ctypes as C
     from paper_2304_09673_b200 import _capi as capi
+    off = (C.c_size_t * 7)()
+    total = C.c_size_t()
+    capi.check(lib.bt_gbuffer_layout(rd.ctx, off, C.byref(total)), "bt_gbuffer_layout")
+
+    def host_set():
+        # one pinned slab per set, planes at bt_gbuffer_layout's offsets: the
+        # download merges them into two copies
+        slab = torch.empty(total.value, dtype=torch.uint8).pin_memory()
+        spec = (("hit", W * H, torch.uint8), ("depth", W * H, torch.float32), ("normal", W * H * 3, torch.float32),
+                ("evalCount", W * H, torch.int32), ("tmo", tx * ty, torch.int32), ("tcb", tx * ty, torch.int32),
+                ("terr", tx * ty, torch.uint8))
+        out = {k: slab[off[i]:off[i] + n * torch.empty(0, dtype=d).element_size()].view(d)
+               for i, (k, n, d) in enumerate(spec)}
+        out["_slab"] = slab
+        return out
+    outs = [host_set(), host_set()]
 
     def step(f, stream_dl):
         w, p, c = frames[f]
@@ -426,7 +436,8 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
         out = outs[f % 2]
         args_ = [C.c_void_p(out[k].data_ptr()) for k in planes]
         if stream_dl:
-            capi.check(lib.bt_gbuffer_download_async(rd.ctx, *args_), "bt_gbuffer_download_async")
+            capi.check(lib.bt_gbuffer_download_async_slab(rd.ctx, C.c_void_p(out["_slab"].data_ptr())),
+                       "bt_gbuffer_download_async_slab")
         else:
             capi.check(lib.bt_gbuffer_download(rd.ctx, *args_), "bt_gbuffer_download")
 
@@ -451,7 +462,7 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
     d2h = W * H * (1 + 4 + 12 + 4) + tx * ty * (4 + 4 + 1)
     return {"value": round(W * H / dt / 1e6, 2), "unit": "Mrays/s", "ms_per_step": round(dt * 1e3, 4),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": "bt_params_update (pinned host) -> bt_render_frame -> bt_gbuffer_download_async (pinned host, "
+            "path": "bt_params_update (pinned host) -> bt_render_frame -> bt_gbuffer_download_async_slab (one pinned host slab, "
                     "copy stream; frame N's D2H overlaps frame N+1's render), wall clock",
             "sync_variant": {"value": round(W * H / dt_sync / 1e6, 2), "ms_per_step": round(dt_sync * 1e3, 4),
                              "path": "same with the blocking bt_gbuffer_download per frame"}}

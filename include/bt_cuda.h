@@ -152,16 +152,22 @@ BT_API int bt_tree_upload(bt_ctx* ctx, const float* data, uint32_t nwords,
                           const bt_node* nodes, uint32_t nnodes,
                           const uint32_t* primitiveWords, uint32_t nprims,
                           uint32_t rootWord);
-/* Per-frame parameter deltas (update_primitive_params, linear_tree.cpp:187-193
- * after host validation): entry i rewrites count[i] floats at
- * data[4*(words[i]+1)] from params[i*stride ...].  Host buffers (H2D inside)
- * or device buffers (_device variant, for the resident fast path). */
 /* compute_fast_indices (linear_tree.cpp:150-168) on the uploaded tree, in
  * place on the device: every blob's ancestor becomes its fast target.  A
  * tree uploaded with parent ancestors (compile() only) ends up bit-identical
  * to one compiled with compute_fast_indices on the host; pointer jumping,
  * O(n log n) work instead of O(n x chain length).  bt_tree_download reads it. */
 BT_API int bt_tree_fast_indices(bt_ctx* ctx);
+/* Per-frame parameter deltas (update_primitive_params, linear_tree.cpp:187-193
+ * after host validation): entry i rewrites count[i] floats at
+ * data[4*(words[i]+1)] from params[i*stride ...].
+ * Host buffers: PINNED ones (cudaHostAlloc / cudaHostRegister) are read by
+ * the update kernel itself over PCIe, in stream order -- no copy-engine
+ * transfer that would queue behind a streamed G-buffer download -- so, as
+ * with any asynchronous copy from pinned memory, they must not change until
+ * the frame has been synchronised.  Pageable buffers are staged with
+ * cudaMemcpyAsync.  The _device variant takes device buffers (resident fast
+ * path). */
 BT_API int bt_params_update(bt_ctx* ctx, const uint32_t* words, const float* params,
                             const uint32_t* counts, uint32_t n, uint32_t stride);
 BT_API int bt_params_update_device(bt_ctx* ctx, const uint32_t* d_words, const float* d_params,
@@ -223,6 +229,15 @@ BT_API int bt_gbuffer_download_async(bt_ctx* ctx, uint8_t* hit, float* depth, fl
                                      uint32_t* evalCount, uint32_t* tileMaxOverlap,
                                      uint32_t* tileCacheBytes, uint8_t* tileError);
 BT_API int bt_download_wait(bt_ctx* ctx);
+/* Byte offsets of the seven planes (hit, depth, normal, evalCount,
+ * tileMaxOverlap, tileCacheBytes, tileError; 16-byte aligned) in one host
+ * slab of `total` bytes for the context's current image size. */
+BT_API int bt_gbuffer_layout(bt_ctx* ctx, size_t offsets[7], size_t* total);
+/* bt_gbuffer_download_async into ONE pinned allocation of at least `total`
+ * bytes, planes at bt_gbuffer_layout's offsets (padding bytes between planes
+ * are not written): adjacent planes go down as one range, two copies per
+ * frame instead of up to fourteen. */
+BT_API int bt_gbuffer_download_async_slab(bt_ctx* ctx, void* slab);
 
 /* Fused gather over peer memory (multi-GPU).  The root rank
  * exports its G-buffer planes as CUDA IPC handles; every other rank imports

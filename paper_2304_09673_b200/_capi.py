@@ -99,6 +99,8 @@ PROTOTYPES = {
     "bt_gbuffer_download": [vp, vp, vp, vp, vp, vp, vp, vp],
     "bt_gbuffer_download_async": [vp, vp, vp, vp, vp, vp, vp, vp],
     "bt_download_wait": [vp],
+    "bt_gbuffer_layout": [vp, P(C.c_size_t), P(C.c_size_t)],
+    "bt_gbuffer_download_async_slab": [vp, vp],
     "bt_set_tile_order": [vp, vp, u32],
     "bt_gbuffer_export": [vp, vp],
     "bt_gbuffer_import": [vp, vp],

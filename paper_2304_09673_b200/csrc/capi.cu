@@ -816,6 +816,27 @@ int bt_params_update(bt_ctx* c, const uint32_t* words, const float* params, cons
         if (words[i] + 1 + (counts[i] + 3) / 4 > c->nwords || counts[i] > stride)
             return fail(BT_EINVAL, "parameter update outside the tree");
     }
+    {  // pinned host buffers: the update kernel reads them over PCIe (see bt_cuda.h)
+        const void* host[3] = {words, params, counts};
+        void* mapped[3] = {};
+        bool ok = true;
+        for (int i = 0; i < 3 && ok; ++i) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, host[i]) != cudaSuccess) {
+                cudaGetLastError();  // clear the query's error: unregistered memory is not a failure
+                ok = false;
+                break;
+            }
+            ok = a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+            mapped[i] = a.devicePointer;
+        }
+        if (ok) {
+            launch_params_update(c->stream, c->words.ptr, static_cast<const uint32_t*>(mapped[0]),
+                                 static_cast<const float*>(mapped[1]), static_cast<const uint32_t*>(mapped[2]), n,
+                                 stride);
+            return BT_OK;
+        }
+    }
     const bool moved = n > c->pWords.cap || (size_t)n * stride > c->pParams.cap;
     BT_CUDA(c->pWords.reserve(n));
     BT_CUDA(c->pCounts.reserve(n));
@@ -1137,9 +1158,18 @@ int bt_gbuffer_download(bt_ctx* c, uint8_t* hit, float* depth, float* normal, ui
     return BT_OK;
 }
 
-int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
-                              uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
-    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+namespace {
+// slab = true: the seven planes lie at bt_gbuffer_layout's offsets of ONE
+// caller allocation, so adjacent planes may be copied as one range (a copy
+// must never span two separately pinned allocations)
+int download_async(bt_ctx* c, void* const* planes, bool slab) {
+    void* hit = planes[0];
+    void* depth = planes[1];
+    void* normal = planes[2];
+    void* evalCount = planes[3];
+    void* tileMaxOverlap = planes[4];
+    void* tileCacheBytes = planes[5];
+    void* tileError = planes[6];
     const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
     // plane layout of a snapshot slot (16-byte aligned offsets)
     const size_t sz[7] = {px, px * 4, px * 12, px * 4, tiles * 4, tiles * 4, tiles};
@@ -1182,21 +1212,81 @@ int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* norm
         launch_copy_segments(c->stream, s7, d7, sz, 7, c->smCount);
     }
     BT_CUDA(cudaEventRecord(c->evSnap[slot], c->stream));
-    // each plane goes down in two halves on two copy streams: one D2H stream
-    // reaches ~33 GB/s on this PCIe link, two concurrent ones ~56 GB/s
-    BT_CUDA(cudaStreamWaitEvent(c->copyStream, c->evSnap[slot], 0));
-    BT_CUDA(cudaStreamWaitEvent(c->copyStream2, c->evSnap[slot], 0));
+    // Host planes laid out like the snapshot slot (bt_gbuffer_layout: one
+    // pinned slab) merge into one contiguous run; the runs then go down split
+    // by bytes over two copy streams -- one D2H stream reaches ~44 GB/s on
+    // this PCIe link, two concurrent ones ~55 GB/s, and every extra copy
+    // costs a few microseconds of DMA setup.
+    struct Run {
+        uint8_t* d;
+        const uint8_t* s;
+        size_t n;
+    };
+    Run runs[7];
+    int nr = 0;
+    size_t bytes = 0;
     for (int i = 0; i < 7; ++i) {
         if (!dst[i]) continue;
-        const size_t h = (sz[i] / 2 + 15) & ~(size_t)15;
-        BT_CUDA(cudaMemcpyAsync(dst[i], base + off[i], h, cudaMemcpyDeviceToHost, c->copyStream));
-        if (sz[i] > h)
-            BT_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst[i]) + h, base + off[i] + h, sz[i] - h,
-                                    cudaMemcpyDeviceToHost, c->copyStream2));
+        uint8_t* d = static_cast<uint8_t*>(dst[i]);
+        const uint8_t* sp = base + off[i];
+        Run& last = runs[nr > 0 ? nr - 1 : 0];
+        if (slab && nr > 0 && (last.n & 15) == 0 && last.d + last.n == d && last.s + last.n == sp) {
+            last.n += sz[i];
+        } else {
+            // a run ending in a padded plane is closed: its padding is not the caller's memory
+            runs[nr++] = Run{d, sp, sz[i]};
+        }
+        bytes += sz[i];
+    }
+    BT_CUDA(cudaStreamWaitEvent(c->copyStream, c->evSnap[slot], 0));
+    BT_CUDA(cudaStreamWaitEvent(c->copyStream2, c->evSnap[slot], 0));
+    const size_t half = (bytes / 2 + 15) & ~(size_t)15;
+    size_t done = 0;
+    for (int r = 0; r < nr; ++r) {
+        const Run& u = runs[r];
+        // bytes of this run that fall in the first half of the total
+        const size_t first = done >= half ? 0 : std::min(u.n, half - done);
+        if (first) BT_CUDA(cudaMemcpyAsync(u.d, u.s, first, cudaMemcpyDeviceToHost, c->copyStream));
+        if (u.n > first)
+            BT_CUDA(cudaMemcpyAsync(u.d + first, u.s + first, u.n - first, cudaMemcpyDeviceToHost, c->copyStream2));
+        done += u.n;
     }
     BT_CUDA(cudaEventRecord(c->evCopied[slot], c->copyStream));
     BT_CUDA(cudaEventRecord(c->evCopied2[slot], c->copyStream2));
     c->dlPending[slot] = true;
+    return BT_OK;
+}
+}  // namespace
+
+int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
+                              uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    void* const planes[7] = {hit, depth, normal, evalCount, tileMaxOverlap, tileCacheBytes, tileError};
+    return download_async(c, planes, false);
+}
+
+int bt_gbuffer_download_async_slab(bt_ctx* c, void* slab) {
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    if (!slab) return fail(BT_EINVAL, "slab is null");
+    size_t off[7], total = 0;
+    const int rc = bt_gbuffer_layout(c, off, &total);
+    if (rc != BT_OK) return rc;
+    void* planes[7];
+    for (int i = 0; i < 7; ++i) planes[i] = static_cast<uint8_t*>(slab) + off[i];
+    return download_async(c, planes, true);
+}
+
+int bt_gbuffer_layout(bt_ctx* c, size_t offsets[7], size_t* total) {
+    if (!c || !offsets || !total) return fail(BT_EINVAL, "null argument");
+    if (c->width <= 0 || c->height <= 0) return fail(BT_ESTATE, "no image size yet (upload a camera or render first)");
+    const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
+    const size_t sz[7] = {px, px * 4, px * 12, px * 4, tiles * 4, tiles * 4, tiles};
+    size_t t = 0;
+    for (int i = 0; i < 7; ++i) {
+        offsets[i] = t;
+        t += (sz[i] + 15) & ~(size_t)15;
+    }
+    *total = t;
     return BT_OK;
 }
 

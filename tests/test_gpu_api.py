@@ -232,6 +232,74 @@ def test_streaming_download_matches_blocking_download(rd):
     assert any(a.depth.tobytes() != b.depth.tobytes() for a, b in zip(reference, reference[1:])), "frames differ"
 
 
+@pytest.mark.parametrize("w,h", [(512, 512), (203, 117)])
+def test_streaming_download_into_one_slab(rd, w, h):
+    """bt_gbuffer_download_async_slab: planes at bt_gbuffer_layout's offsets
+    of one pinned slab go down as merged runs (two copies): identical to the blocking download,
+    including odd image sizes whose planes are not 16-byte multiples (their
+    padding is never written), and the bytes between planes stay untouched."""
+    import ctypes as C
+
+    import torch
+    cfg = RenderConfig()
+    s = Scene.build("C1", 0, w, h)
+    rd.upload(s)
+    cam = s.device_camera
+    rd.render_frame(cam, cfg, exact=False, graph=False)
+    off = (C.c_size_t * 7)()
+    total = C.c_size_t()
+    assert rd.lib.bt_gbuffer_layout(rd.ctx, off, C.byref(total)) == 0
+    tx, ty = s.tiles
+    sizes = [w * h, w * h * 4, w * h * 12, w * h * 4, tx * ty * 4, tx * ty * 4, tx * ty]
+    assert all(off[i] + sizes[i] <= (off[i + 1] if i < 6 else total.value) for i in range(7))
+    assert all(o % 16 == 0 for o in off)
+    slab = torch.full((total.value + 64,), 0xA5, dtype=torch.uint8).pin_memory()
+    for f in range(3):
+        wv, p, c = s.perturb(f)
+        rd.update_params(wv, p, c)
+        rd.render_frame(cam, cfg, exact=False, graph=True)
+        assert rd.lib.bt_gbuffer_download_async_slab(rd.ctx, C.c_void_p(slab.data_ptr())) == 0
+        g = rd.download_gbuffer()
+        assert rd.lib.bt_download_wait(rd.ctx) == 0
+        b = slab.numpy()
+        planes = [g.hit, g.depth, g.normal, g.evalCount, g.tileMaxOverlap, g.tileCacheBytes, g.tileError]
+        for i, pl in enumerate(planes):
+            raw = np.ascontiguousarray(pl).tobytes()
+            assert len(raw) == sizes[i]
+            assert b[off[i]:off[i] + sizes[i]].tobytes() == raw, f"plane {i}"
+            end = off[i + 1] if i < 6 else total.value + 64
+            assert (b[off[i] + sizes[i]:end] == 0xA5).all(), f"padding after plane {i} written"
+
+
+def test_params_update_from_pinned_host_equals_pageable(rd):
+    """bt_params_update reads PINNED host buffers with the update kernel
+    itself (no copy engine); pageable buffers are staged.  Both give the
+    same tree words, frame after frame, and the same rendered frame."""
+    import ctypes as C
+
+    import torch
+    s = Scene.build("C3", 0, 320, 180)
+    cfg = RenderConfig()
+    trees, frames = [], []
+    for pinned in (False, True):
+        rd.upload(s)
+        for f in range(3):
+            w, p, c = s.perturb(f)
+            if pinned:
+                tw, tp, tc = (torch.from_numpy(a.view(np.int32) if a.dtype != np.float32 else a).pin_memory()
+                              for a in (w, p, c))
+                assert rd.lib.bt_params_update(rd.ctx, C.c_void_p(tw.data_ptr()), C.c_void_p(tp.data_ptr()),
+                                               C.c_void_p(tc.data_ptr()), len(w), 17) == 0
+                assert rd.lib.bt_sync(rd.ctx) == 0  # the pinned buffers are read in stream order
+            else:
+                rd.update_params(w, p, c)
+        trees.append(rd.tree_words())
+        rd.render_frame(s.device_camera, cfg, exact=True, graph=False)
+        frames.append(rd.download_gbuffer())
+    assert trees[0].tobytes() == trees[1].tobytes()
+    assert frames[0].depth.tobytes() == frames[1].depth.tobytes()
+
+
 def test_march_schedule_never_changes_results(rd):
     """Raster order, the device's longest-first order with half-tile units
     (mode 1) and a random host permutation give bit-identical frames and
