@@ -33,7 +33,10 @@ namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kTraceWarps = 4;
 constexpr int kFullStackCap = 128;
-constexpr uint32_t kMarchBlocks = 320;  // float4s of fast parameter blocks kept in shared memory per warp
+#ifndef BT_MARCH_BLOCKS
+#define BT_MARCH_BLOCKS 320
+#endif
+constexpr uint32_t kMarchBlocks = BT_MARCH_BLOCKS;  // float4s of fast parameter blocks kept in shared memory per warp
 constexpr uint32_t kNoRay = 0xFFFFFFFFu;
 
 template <class O> __device__ __forceinline__ F3 ray_point(F3 o, F3 d, float t) {
@@ -682,7 +685,7 @@ int trace_min_blocks() {
         mb = kDefaultMinBlocks;
         if (const char* e = getenv("BT_TRACE_MINBLOCKS")) {
             const int v = atoi(e);
-            if (v == 4 || v == 5 || v == 6 || v == 8) mb = v;
+            if (v >= 4 && v <= 8) mb = v;
         }
     }
     return mb;
@@ -693,6 +696,7 @@ void* trace_fn(bool exact) {
         case 4: return TraceVariant<4>::fn(exact);
         case 5: return TraceVariant<5>::fn(exact);
         case 6: return TraceVariant<6>::fn(exact);
+        case 7: return TraceVariant<7>::fn(exact);
         default: return TraceVariant<8>::fn(exact);
     }
 }
