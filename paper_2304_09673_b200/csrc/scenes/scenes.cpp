@@ -356,6 +356,15 @@ std::unique_ptr<Scene> build(const std::string& name, uint32_t seed, int width, 
         SceneDocument doc = generate_synthetic(f[1], static_cast<uint32_t>(std::stoul(f[2])), f[3], f[4], seed);
         root = std::move(doc.root);
         sc->camera = doc.camera;
+    } else if (name.rfind("stack:", 0) == 0) {  // n nearly concentric spheres, balanced compact unions:
+        // every tile on the silhouette sees n overlapping fragments (overlap saturation, view overflow)
+        const uint32_t n = static_cast<uint32_t>(std::stoul(name.substr(6)));
+        if (n == 0) throw std::invalid_argument("stack:<n> needs n >= 1");
+        std::vector<NodePtr> units;
+        for (uint32_t i = 0; i < n; ++i)
+            units.push_back(prim(PrimitiveParams::sphere(1.0f + 0.002f * i, Transform{{0.001f * i, 0, 0}, Quat{}})));
+        root = balanced(units, 0, units.size());
+        sc->camera = look_at(Vec3{0, 0, -6}, origin, 0.1f, 40.0f, 64, 64);
     } else if (name.rfind("random:", 0) == 0) {
         const uint32_t n = static_cast<uint32_t>(std::stoul(name.substr(7)));
         Rng r(seed ? seed : 7u);
@@ -449,6 +458,29 @@ __attribute__((visibility("default"))) void SC_FN(scene_camera)(void* h, float* 
                          c.target.z,   c.up.x,       c.up.y,       c.up.z,     c.fovDegrees,
                          c.nearZ,      c.farZ,       (float)c.width, (float)c.height};
     std::memcpy(out, v, sizeof(v));
+}
+
+// Replace the camera (same 14 floats as scene_camera); validated like every
+// camera.  Edge-case tests: cameras looking away from the scene, inside its
+// volumes, with the scene beyond the far plane, sub-tile images.
+__attribute__((visibility("default"))) int SC_FN(scene_set_camera)(void* h, const float* v) {
+    blobtree::Camera c;
+    c.position = blobtree::Vec3{v[0], v[1], v[2]};
+    c.target = blobtree::Vec3{v[3], v[4], v[5]};
+    c.up = blobtree::Vec3{v[6], v[7], v[8]};
+    c.fovDegrees = v[9];
+    c.nearZ = v[10];
+    c.farZ = v[11];
+    c.width = static_cast<int>(v[12]);
+    c.height = static_cast<int>(v[13]);
+    try {
+        blobtree::validate_camera(c);
+    } catch (const std::exception& e) {
+        g_sceneError = e.what();
+        return -1;
+    }
+    static_cast<scenes::Scene*>(h)->camera = c;
+    return 0;
 }
 
 // Apply frame `frame` of the C3/C4 perturbation to the scene's own tree and

@@ -41,6 +41,7 @@ def _scenes_lib() -> C.CDLL:
         lib.sc_scene_camera.argtypes = [C.c_void_p, C.c_void_p]
         lib.sc_scene_device_camera.argtypes = [C.c_void_p, C.POINTER(bt_camera)]
         lib.sc_scene_perturb.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.sc_scene_set_camera.argtypes = [C.c_void_p, C.c_void_p]
         lib.sc_scene_perturb.restype = C.c_uint32
         _scenes = lib
     return _scenes
@@ -128,6 +129,18 @@ class Scene:
     @property
     def tiles(self) -> tuple[int, int]:
         return (self.width + 7) // 8, (self.height + 7) // 8
+
+    def set_camera(self, camera14) -> None:
+        """Replace the camera: position[3] target[3] up[3] fov near far width height."""
+        v = np.ascontiguousarray(camera14, np.float32)
+        lib = _scenes_lib()
+        if lib.sc_scene_set_camera(self.handle, ptr(v)) != 0:
+            raise ValueError(f"camera: {lib.sc_scene_error().decode()}")
+        lib.sc_scene_camera(self.handle, ptr(self.camera14))
+        self.width, self.height = int(v[12]), int(v[13])
+        dc = bt_camera()
+        lib.sc_scene_device_camera(self.handle, C.byref(dc))
+        self.device_camera = dc
 
     def perturb(self, frame: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         """C3/C4 per-frame perturbation; returns (words, params[n,17], counts)."""

@@ -42,6 +42,7 @@ def ref_lib() -> C.CDLL:
         lib.ref_scene_tree.argtypes = [vp, vp, vp, vp]
         lib.ref_scene_camera.argtypes = [vp, vp]
         lib.ref_scene_perturb.argtypes = [vp, C.c_uint32, vp, vp, vp]
+        lib.ref_scene_set_camera.argtypes = [vp, vp]
         lib.ref_scene_perturb.restype = C.c_uint32
         lib.ref_roi.argtypes = [vp, vp]
         lib.ref_vois.argtypes = [vp, C.c_float, vp]
@@ -95,6 +96,12 @@ class RefScene:
         prims = np.zeros(self.nprims, np.uint32)
         ref_lib().ref_scene_tree(self.h, ptr(data), ptr(nodes), ptr(prims))
         return data, nodes, prims
+
+    def set_camera(self, camera14) -> None:
+        v = np.ascontiguousarray(camera14, np.float32)
+        if ref_lib().ref_scene_set_camera(self.h, ptr(v)) != 0:
+            raise ValueError(ref_lib().ref_scene_error().decode())
+        self.width, self.height = int(v[12]), int(v[13])
 
     def camera14(self) -> np.ndarray:
         c = np.zeros(14, np.float32)

@@ -19,6 +19,7 @@ import os
 import numpy as np
 import pytest
 
+from edge_cases import EDGE
 from oracle_bridge import Port, RefScene, ref_available
 from paper_2304_09673_b200.pipeline import FRAG_DTYPE, VOI_DTYPE, RenderConfig, Renderer, Scene
 
@@ -38,8 +39,10 @@ def same(a, b):
 class Checker:
     """Reference (preferred) or C restatement on the same scene."""
 
-    def __init__(self, scene: Scene, name, seed, w, h):
+    def __init__(self, scene: Scene, name, seed, w, h, camera14=None):
         self.ref = RefScene(name, seed, w, h) if ref_available() else None
+        if self.ref is not None and camera14 is not None:
+            self.ref.set_camera(camera14)
         self.port = Port.from_scene(scene)
 
     def roi(self):
@@ -261,4 +264,41 @@ def test_exact_pipeline_stress_configs(rd, name, w, h, over):
     rd.render_frame(cam, cfg, exact=False, graph=False)
     gf = rd.download_gbuffer()
     assert (gf.hit == g.hit).mean() >= 0.999
+    assert (gf.tileError == g.tileError).all()
+
+
+@pytest.mark.parametrize("name,cam14,what", EDGE, ids=[e[2] for e in EDGE])
+def test_exact_pipeline_edge_cameras(rd, name, cam14, what):
+    """Degenerate cameras and images: the A-buffer, every G-buffer plane and
+    RenderStats stay bit-identical to the reference, and the FMA path agrees
+    on hits and tile errors."""
+    cfg = RenderConfig()
+    s = Scene.build(name)
+    s.set_camera(cam14)
+    chk = Checker(s, name, 0, 0, 0, camera14=cam14)
+    rd.upload(s)
+    cam = s.device_camera
+    vois = rd.build_volumes_of_interest(cfg.hitEpsilon)
+    vois_ref = chk.vois(cfg.hitEpsilon)
+    assert same(vois, vois_ref)
+    off, frags = rd.rasterize_volumes(cam)
+    off_ref, frags_ref = chk.rasterize(vois_ref)
+    assert same(off, off_ref) and same(frags, frags_ref)
+    rd.reset_stats()
+    rd.render_tiles(cam, cfg, exact=True)
+    rd.compute_normals(cam, cfg.normalsMode, exact=True)
+    g = rd.download_gbuffer()
+    st = rd.stats()
+    gr, st_ref = chk.render(cfg, off_ref, frags_ref)
+    for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+        assert same(getattr(g, plane), getattr(gr, plane)), plane
+    assert [st.fieldEvals, st.retainedNodeVisits, st.primitiveEvals, st.treeNodeCount, st.maxOverlap,
+            st.maxCacheBytes] == st_ref
+    if what.startswith("looking away") or what.startswith("whole scene"):
+        assert len(frags) == 0 and not g.hit.any()
+    if what.startswith("overlap saturation"):
+        assert st.maxOverlap == cfg.maxOverlap and st.maxCacheBytes == 3072  # both caps reached
+    rd.render_frame(cam, cfg, exact=False, graph=True)  # graph-replayed FMA path on the same camera
+    gf = rd.download_gbuffer()
+    assert (gf.hit == g.hit).mean() >= 0.99
     assert (gf.tileError == g.tileError).all()
