@@ -119,7 +119,11 @@ void launch_params_update(cudaStream_t st, float4* words, const uint32_t* dWords
                           uint32_t stride);
 void launch_roi_all(cudaStream_t st, const DevTree& t, float* roi);
 void launch_voi(cudaStream_t st, const DevTree& t, const float* roi, float margin, Voi* vois);
-void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY);
+// rays, tile cones and pyramids of the superblock rows meeting [tile0, tile1)
+void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0,
+                   uint32_t tile1);
+// tiles [*cover0, return) whose rays launch_camera(tile0, tile1) computes
+uint32_t camera_tile_cover(int tilesX, int tilesY, uint32_t tile0, uint32_t tile1, uint32_t* cover0);
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
                     const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
                     int smCount);

@@ -108,6 +108,7 @@ struct bt_ctx {
     bool haveAbuffer = false;
     bool haveRays = false;
     bt_camera rayCam{};
+    uint32_t rayT0 = 0, rayT1 = 0;  // tiles whose rays / cones are current (whole superblock rows)
 
     // G-buffer
     DevBuf<uint8_t> hit, tileError;
@@ -380,13 +381,26 @@ int check_config(const bt_render_config* cfg) {
     return BT_OK;
 }
 
-int do_camera(bt_ctx* c, const bt_camera& cam) {
+// Rays, tile cones and pyramids for the superblock rows that meet
+// [tile0, tile1) (tile1 == 0: the whole image).  A sharded rank that does not
+// compute normals needs only its own rows.
+int do_camera(bt_ctx* c, const bt_camera& cam, uint32_t tile0 = 0, uint32_t tile1 = 0) {
     int rc = ensure_image(c, cam);
     if (rc) return rc;
-    launch_camera(c->stream, to_cam(cam), frame_bufs(c), c->tilesX, c->tilesY);
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    if (tile1 == 0 || tile1 > tiles) tile1 = tiles;
+    if (tile0 > tile1) tile0 = tile1;
+    launch_camera(c->stream, to_cam(cam), frame_bufs(c), c->tilesX, c->tilesY, tile0, tile1);
     c->haveRays = true;
     c->rayCam = cam;
+    c->rayT1 = camera_tile_cover(c->tilesX, c->tilesY, tile0, tile1, &c->rayT0);
     return BT_OK;
+}
+
+// true when the current rays cover [tile0, tile1) for this camera
+bool rays_cover(const bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1) {
+    return c->haveRays && std::memcmp(&c->rayCam, &cam, sizeof(bt_camera)) == 0 && c->rayT0 <= tile0 &&
+           tile1 <= c->rayT1;
 }
 
 int resolve_tiles(bt_ctx* c, uint32_t& tile0, uint32_t& tile1) {
@@ -939,9 +953,11 @@ int bt_abuffer_build(bt_ctx* c, const bt_camera* cam, uint32_t tile0, uint32_t t
     int rc = check_camera(cam);
     if (rc) return rc;
     prof_begin(c);
-    rc = do_camera(c, *cam);
+    rc = ensure_image(c, *cam);
     if (rc) return rc;
     rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    rc = do_camera(c, *cam, tile0, tile1);
     if (rc) return rc;
     rc = do_abuffer(c, *cam, tile0, tile1, true);
     prof_end(c, 1);
@@ -1011,11 +1027,12 @@ int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint3
     if (!c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
     if (cam->width != c->width || cam->height != c->height)
         return fail(BT_EINVAL, "camera image size differs from the A-buffer's");
-    if (!c->haveRays || std::memcmp(&c->rayCam, cam, sizeof(bt_camera)) != 0) {
+    rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    if (!rays_cover(c, *cam, tile0, tile1)) {
         rc = do_camera(c, *cam);
         if (rc) return rc;
     }
-    rc = resolve_tiles(c, tile0, tile1);
     if (rc) return rc;
     prof_begin(c);
     rc = do_trace(c, *cam, *cfg, tile0, tile1, exact, true);
@@ -1029,6 +1046,10 @@ int bt_normals(bt_ctx* c, const bt_camera* cam, int mode, int exact) {
     if (rc) return rc;
     if (mode != 0 && mode != 1) return fail(BT_EINVAL, "unknown normals mode");
     prof_begin(c);
+    if (!rays_cover(c, *cam, 0, (uint32_t)(c->tilesX * c->tilesY))) {  // e.g. after a sharded, normal-less frame
+        rc = do_camera(c, *cam);
+        if (rc) return rc;
+    }
     rc = do_normals(c, *cam, mode, exact);
     prof_end(c, 3);
     return rc;
@@ -1073,7 +1094,8 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         launch_voi(c->stream, dev_tree(c), c->roi.ptr, cfg->hitEpsilon, c->vois.ptr);
         c->haveRoi = true;
         c->nvoi = c->nprims;
-        int r = do_camera(c, *cam);
+        // normals need every ray of the image (they run over the assembled frame)
+        int r = normals ? do_camera(c, *cam) : do_camera(c, *cam, tile0, tile1);
         if (r) return r;
         r = do_abuffer(c, *cam, tile0, tile1, checked);
         if (r) return r;

@@ -173,12 +173,13 @@ __device__ __forceinline__ bool volume_pyramid_may_touch(const float4* pl, F3 ap
 
 // One CTA per superblock: 4096 rays, 64 tile cones, 1 conservative
 // superblock cone containing all of its tile cones.
-__global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY) {
+__global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY, int sb0) {
     __shared__ float4 sCone[64];
     __shared__ float sSin[64];
     __shared__ int sValid[64];
     const int sbX = (tilesX + kSB - 1) / kSB;
-    const int sx = blockIdx.x % sbX, sy = blockIdx.x / sbX;
+    const int sb = sb0 + (int)blockIdx.x;
+    const int sx = sb % sbX, sy = sb / sbX;
     for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
         const int lt = k >> 6, pix = k & 63;
         const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tiles
     if (threadIdx.x == 64) {
         const int x0 = sx * kSB * kTile, y0 = sy * kSB * kTile;
         const int x1 = min(x0 + kSB * kTile, cam.width) - 1, y1 = min(y0 + kSB * kTile, cam.height) - 1;
-        pixel_pyramid(cam, x0, y0, x1, y1, fb.sbFrustum + (size_t)blockIdx.x * 4);
+        pixel_pyramid(cam, x0, y0, x1, y1, fb.sbFrustum + (size_t)sb * 4);
     }
     __syncthreads();
     // superblock cone: axis = normalized sum of tile axes, half-angle =
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tiles
             // absolute + relative padding: float rounding of the exact tile
             // test is ~1e-6 relative, the pad is two orders above it.
             th = th * 1.0001f + 2e-4f;
-            fb.sbCones[blockIdx.x] = make_float4(ax, ay, az, th);
+            fb.sbCones[sb] = make_float4(ax, ay, az, th);
         }
     }
 }
@@ -272,7 +273,7 @@ __device__ __forceinline__ bool sb_may_touch(float4 sc, F3 apex, const Sphere& s
 // coarse superblock cull; surviving (volume, superblock) pairs are appended.
 __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_t nvoi, FrameBufs fb,
                                                 int tilesX, int tilesY, uint32_t tile0,
-                                                uint32_t tile1) {
+                                                uint32_t tile1, int sbLo, int sbHi) {
     // warp = (volume, chunk of 32 superblocks): grid.y runs over the chunks
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -282,12 +283,12 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
     const float vz = view_z(cam, bs.c);
     if (E::add(vz, bs.r) < cam.nearZ || E::sub(vz, bs.r) > cam.farZ) return;
     const VolumeSupport sup = volume_support(v, cam.pos);
-    const int sbX = (tilesX + kSB - 1) / kSB, sbY = (tilesY + kSB - 1) / kSB;
-    const int nsb = sbX * sbY;
-    for (int base = 32 * blockIdx.y; base < nsb; base += 32 * gridDim.y) {
+    const int sbX = (tilesX + kSB - 1) / kSB;
+    // superblocks [sbLo, sbHi): the rows of superblocks that meet [tile0, tile1)
+    for (int base = sbLo + 32 * (int)blockIdx.y; base < sbHi; base += 32 * (int)gridDim.y) {
         const int sb = base + lane;
         bool pass = false;
-        if (sb < nsb) {
+        if (sb < sbHi) {
             const int sx = sb % sbX, sy = sb / sbX;
             const uint32_t first = (uint32_t)(sy * kSB * tilesX + sx * kSB);
             const int lastTy = min(sy * kSB + kSB, tilesY) - 1, lastTx = min(sx * kSB + kSB, tilesX) - 1;
@@ -519,16 +520,17 @@ __device__ __forceinline__ bool key_less(const uint4& a, const uint4& b) {
 
 constexpr int kSortStage = 256;
 
-__global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles) {
+// Warp per tile of [first, last) (the frame's tile range).
+__global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles, uint32_t first, uint32_t last) {
     __shared__ uint4 stage[4][kSortStage];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x * 4 + wid;
-    if (tile >= tiles) return;
+    const uint32_t tile = first + blockIdx.x * 4 + wid;
+    if (tile >= last) return;
     if (pool_overflowed(fb)) {  // never index past the pool: empty A-buffer, flagged
         if (lane == 0) {
             fb.offsets[tile] = 0;
             if (tile == tiles - 1) fb.offsets[tiles] = 0;
-            if (tile == 0) atomicExch(&fb.counters[kCntOverflow], 1u);
+            if (tile == first) atomicExch(&fb.counters[kCntOverflow], 1u);
         }
         return;
     }
@@ -553,6 +555,17 @@ __global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles) {
         f.zExit = __uint_as_float(me.z);
         fb.frags[off + rank] = f;
     }
+}
+
+// CSR offsets of every tile, thread per tile: a sharded frame sorts only its
+// own tile range, the other tiles are empty but keep valid offsets.
+__global__ void k_offsets_all(FrameBufs fb, uint32_t tiles) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tiles) return;
+    const bool ov = pool_overflowed(fb);
+    const uint32_t off = ov ? 0u : tile_offset(fb, t);
+    fb.offsets[t] = off;
+    if (t == tiles - 1) fb.offsets[tiles] = ov ? 0u : off + fb.tileCount[t];
 }
 
 __global__ void k_offsets_from_counts(FrameBufs fb, uint32_t tiles) {
@@ -583,9 +596,32 @@ void launch_voi(cudaStream_t st, const DevTree& t, const float* roi, float margi
     k_voi<<<(t.nprims + 127) / 128, 128, 0, st>>>(t, roi, margin, vois);
 }
 
-void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY) {
-    const int nsb = ((tilesX + kSB - 1) / kSB) * ((tilesY + kSB - 1) / kSB);
-    k_camera<<<nsb, 256, 0, st>>>(cam, fb, tilesX, tilesY);
+// Superblocks [sbLo, sbHi) whose rows meet the tile range [tile0, tile1).
+static void sb_range(int tilesX, int tilesY, uint32_t tile0, uint32_t tile1, int& sbLo, int& sbHi) {
+    const int sbX = (tilesX + kSB - 1) / kSB, sbY = (tilesY + kSB - 1) / kSB;
+    if (tile1 <= tile0) {
+        sbLo = sbHi = 0;
+        return;
+    }
+    const int row0 = (int)(tile0 / (uint32_t)tilesX) / kSB, row1 = (int)((tile1 - 1) / (uint32_t)tilesX) / kSB + 1;
+    sbLo = row0 * sbX;
+    sbHi = std::min(row1, sbY) * sbX;
+}
+
+uint32_t camera_tile_cover(int tilesX, int tilesY, uint32_t tile0, uint32_t tile1, uint32_t* cover0) {
+    int sbLo, sbHi;
+    sb_range(tilesX, tilesY, tile0, tile1, sbLo, sbHi);
+    const int sbX = (tilesX + kSB - 1) / kSB;
+    const uint32_t tiles = (uint32_t)(tilesX * tilesY);
+    *cover0 = std::min<uint32_t>(tiles, (uint32_t)(sbLo / sbX) * kSB * (uint32_t)tilesX);
+    return std::min<uint32_t>(tiles, (uint32_t)(sbHi / sbX) * kSB * (uint32_t)tilesX);
+}
+
+void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0,
+                   uint32_t tile1) {
+    int sbLo, sbHi;
+    sb_range(tilesX, tilesY, tile0, tile1, sbLo, sbHi);
+    if (sbHi > sbLo) k_camera<<<sbHi - sbLo, 256, 0, st>>>(cam, fb, tilesX, tilesY, sbLo);
 }
 
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
@@ -596,19 +632,28 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
     cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
     cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
     if (nvoi > 0) {
-        const uint32_t nsb = (uint32_t)(((tilesX + kSB - 1) / kSB) * ((tilesY + kSB - 1) / kSB));
+        int sbLo, sbHi;
+        sb_range(tilesX, tilesY, tile0, tile1, sbLo, sbHi);
+        const uint32_t nsb = (uint32_t)(sbHi - sbLo);
         // enough (volume, chunk) warps to fill the GPU (~16k), no more: each
         // warp repeats the volume's setup
-        const uint32_t chunks = std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 16384u / nvoi));
+        const uint32_t chunks =
+            std::max<uint32_t>(1u, std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 16384u / nvoi)));
         const dim3 grid((nvoi * 32 + 255) / 256, chunks);
-        k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1);
+        k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1, sbLo, sbHi);
         k_tiles<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
         k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb);
     }
     const uint32_t nblocks = (tiles + kScanBlock - 1) / kScanBlock;
     k_scan<<<nblocks, 1024, 0, st>>>(fb, tiles);
     k_scatter<<<smCount * 4, 256, 0, st>>>(vois, fb);
-    k_sort<<<(tiles + 3) / 4, 128, 0, st>>>(fb, tiles);
+    if (tile0 == 0 && tile1 >= tiles) {
+        k_sort<<<(tiles + 3) / 4, 128, 0, st>>>(fb, tiles, 0u, tiles);
+    } else {
+        k_offsets_all<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
+        const uint32_t last = std::min(tile1, tiles);
+        if (last > tile0) k_sort<<<(last - tile0 + 3) / 4, 128, 0, st>>>(fb, tiles, tile0, last);
+    }
 }
 
 void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles) {

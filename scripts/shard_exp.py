@@ -44,6 +44,24 @@ for n in (2, 4, 8):
                                                   normals=False)))
     print(name, n, "ranks: per-rank ms", np.round(per, 4), f"max {max(per):.4f} -> ideal speed-up {full / max(per):.2f}")
 
+# cost-balanced split: per-row cost = the full frame's evaluation count of the
+# row (what the bench's multi-GPU path measures in its warm-up frames)
+rd.render_frame(cam, cfg, exact=False, graph=False)
+g = rd.download_gbuffer()
+ev = np.zeros((ty * 8, tx * 8), np.float64)
+ev[:s.height, :s.width] = g.evalCount.reshape(s.height, s.width)
+row_cost = ev.reshape(ty, 8, tx * 8).sum(axis=(1, 2))
+for n in (2, 4, 8):
+    for label, cost in (("evals", row_cost), ("evals+tiles", row_cost + row_cost.sum() / ty * 0.25)):
+        rows = tile_row_ranges(ty, n, cost)
+        per = []
+        for r in range(n):
+            t0, t1 = int(rows[r] * tx), int(rows[r + 1] * tx)
+            per.append(timed(lambda: rd.render_frame(cam, cfg, exact=False, graph=True, tile0=t0, tile1=t1,
+                                                      normals=False)))
+        print(name, n, f"ranks balanced by {label}: per-rank ms", np.round(per, 4),
+              f"max {max(per):.4f} -> ideal speed-up {full / max(per):.2f}")
+
 # stage split of one middle rank at 8-way (eager frames, CUDA-event profile)
 import ctypes as C  # noqa: E402
 from paper_2304_09673_b200 import _capi as capi  # noqa: E402
