@@ -20,6 +20,7 @@
 // O = ExactOps gives bit-identical results to the CPU reference; O = FastOps
 // lets nvcc contract the field arithmetic into FFMA (tolerance path).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "bt_device.h"
@@ -61,6 +62,11 @@ template <class O> struct IsFast {
 template <> struct IsFast<FastOps> {
     static constexpr bool value = true;
 };
+
+#ifdef BT_STEP_HIST
+__device__ unsigned long long g_stepHist[33];
+__device__ unsigned int g_stepDone;
+#endif
 
 // Per-warp shared memory of k_march.
 struct MarchSmem {
@@ -124,6 +130,12 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
             continue;
         }
         ++steps;
+#ifdef BT_STEP_HIST
+        {  // experiment (scripts/step_hist.sh): histogram of active lanes per lockstep step
+            const uint32_t act = __ballot_sync(kFull, march_phase(m) != 0u);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&g_stepHist[__popc(act)], 1ull);
+        }
+#endif
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
         if (IsFast<O>::value && fits) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
@@ -289,6 +301,20 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
         march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
     __syncthreads();
+#ifdef BT_STEP_HIST
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_stepDone, 1u) == gridDim.x - 1) {
+            printf("STEPHIST");
+            for (int k = 0; k <= 32; ++k) {
+                printf(" %llu", g_stepHist[k]);
+                g_stepHist[k] = 0;
+            }
+            printf("\n");
+            g_stepDone = 0;
+        }
+    }
+#endif
     if (threadIdx.x == 0) {
         unsigned long long* st = reinterpret_cast<unsigned long long*>(stats);
         if (bs.fe) {
