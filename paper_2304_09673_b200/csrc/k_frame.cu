@@ -269,8 +269,40 @@ __device__ __forceinline__ bool sb_may_touch(float4 sc, F3 apex, const Sphere& s
     return cs * y - sn * x <= s.r + pad;
 }
 
+// Superblock rectangle [x0, x1) x [y0, y1) that contains the screen
+// projection of a bounding sphere, conservatively: the tangent slopes of the
+// sphere seen from the camera (in double, radius and rectangle padded far
+// beyond float rounding of the pixel rays).  A sphere reaching the camera
+// plane keeps the whole screen.  Only a superset filter: the per-superblock
+// pyramid / cone culls and the exact tile tests decide.
+__device__ void sphere_sb_rect(const Cam& c, const Sphere& s, int tilesX, int tilesY, int& x0, int& x1, int& y0,
+                               int& y1) {
+    const int sbX = (tilesX + kSB - 1) / kSB, sbY = (tilesY + kSB - 1) / kSB;
+    x0 = 0, x1 = sbX, y0 = 0, y1 = sbY;
+    const double vx = (double)s.c.x - c.pos.x, vy = (double)s.c.y - c.pos.y, vz = (double)s.c.z - c.pos.z;
+    const double X = vx * c.right.x + vy * c.right.y + vz * c.right.z;
+    const double Y = vx * c.up.x + vy * c.up.y + vz * c.up.z;
+    const double Z = vx * c.fwd.x + vy * c.fwd.y + vz * c.fwd.z;
+    const double R = fabs((double)s.r) * 1.001 + 1e-4 + 1e-4 * sqrt(X * X + Y * Y + Z * Z);
+    if (!(Z > 1.01 * R + 1e-6)) return;
+    const double den = Z * Z - R * R;
+    const double dx = sqrt(X * X + den), dy = sqrt(Y * Y + den);
+    const double ka = (double)c.tanHalf * c.aspect, kb = (double)c.tanHalf;
+    const double pad = 2.0 * kTile;  // pixels
+    const double px0 = ((X * Z - R * dx) / den / ka + 1.0) * 0.5 * c.width - 0.5 - pad;
+    const double px1 = ((X * Z + R * dx) / den / ka + 1.0) * 0.5 * c.width - 0.5 + pad;
+    const double py0 = (1.0 - (Y * Z + R * dy) / den / kb) * 0.5 * c.height - 0.5 - pad;
+    const double py1 = (1.0 - (Y * Z - R * dy) / den / kb) * 0.5 * c.height - 0.5 + pad;
+    const double sbPx = (double)(kSB * kTile);
+    x0 = (int)fmax(0.0, floor(px0 / sbPx));
+    x1 = (int)fmin((double)sbX, floor(px1 / sbPx) + 1.0);
+    y0 = (int)fmax(0.0, floor(py0 / sbPx));
+    y1 = (int)fmin((double)sbY, floor(py1 / sbPx) + 1.0);
+}
+
 // one warp per volume: near/far cull (abuffer.cpp:188-191), then the
-// coarse superblock cull; surviving (volume, superblock) pairs are appended.
+// coarse superblock cull over the superblocks its bounding sphere projects
+// onto; surviving (volume, superblock) pairs are appended.
 __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_t nvoi, FrameBufs fb,
                                                 int tilesX, int tilesY, uint32_t tile0,
                                                 uint32_t tile1, int sbLo, int sbHi) {
@@ -284,12 +316,19 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
     if (E::add(vz, bs.r) < cam.nearZ || E::sub(vz, bs.r) > cam.farZ) return;
     const VolumeSupport sup = volume_support(v, cam.pos);
     const int sbX = (tilesX + kSB - 1) / kSB;
-    // superblocks [sbLo, sbHi): the rows of superblocks that meet [tile0, tile1)
-    for (int base = sbLo + 32 * (int)blockIdx.y; base < sbHi; base += 32 * (int)gridDim.y) {
-        const int sb = base + lane;
+    int rx0, rx1, ry0, ry1;
+    sphere_sb_rect(cam, bs, tilesX, tilesY, rx0, rx1, ry0, ry1);
+    // ... within the superblock rows [sbLo, sbHi) that meet [tile0, tile1)
+    ry0 = max(ry0, sbLo / sbX);
+    ry1 = min(ry1, sbHi / sbX);
+    const int rw = rx1 - rx0, nrect = (rw > 0 && ry1 > ry0) ? rw * (ry1 - ry0) : 0;
+    for (int base = 32 * (int)blockIdx.y; base < nrect; base += 32 * (int)gridDim.y) {
+        const int idx = base + lane;
         bool pass = false;
-        if (sb < sbHi) {
-            const int sx = sb % sbX, sy = sb / sbX;
+        int sb = 0;
+        if (idx < nrect) {
+            const int sx = rx0 + idx % rw, sy = ry0 + idx / rw;
+            sb = sy * sbX + sx;
             const uint32_t first = (uint32_t)(sy * kSB * tilesX + sx * kSB);
             const int lastTy = min(sy * kSB + kSB, tilesY) - 1, lastTx = min(sx * kSB + kSB, tilesX) - 1;
             const uint32_t last = (uint32_t)(lastTy * tilesX + lastTx);
@@ -635,10 +674,11 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
         int sbLo, sbHi;
         sb_range(tilesX, tilesY, tile0, tile1, sbLo, sbHi);
         const uint32_t nsb = (uint32_t)(sbHi - sbLo);
-        // enough (volume, chunk) warps to fill the GPU (~16k), no more: each
-        // warp repeats the volume's setup
+        // (volume, chunk) warps: a volume's superblock rectangle is usually a
+        // few superblocks, so chunks only help when there are few volumes
+        // (each chunk warp repeats the volume's setup and rectangle)
         const uint32_t chunks =
-            std::max<uint32_t>(1u, std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 16384u / nvoi)));
+            std::max<uint32_t>(1u, std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 2048u / nvoi)));
         const dim3 grid((nvoi * 32 + 255) / 256, chunks);
         k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1, sbLo, sbHi);
         k_tiles<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
