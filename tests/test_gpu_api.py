@@ -300,6 +300,45 @@ def test_params_update_from_pinned_host_equals_pageable(rd):
     assert frames[0].depth.tobytes() == frames[1].depth.tobytes()
 
 
+def test_frames_in_flight_equal_back_to_back_frames(rd):
+    """Two contexts on their own streams rendering alternate frames of a
+    perturbed sequence concurrently (bench.py's frames_in_flight) give the
+    frames a single context renders back to back, bit for bit."""
+    import torch
+    s = Scene.build("C3", 0, 480, 270)
+    cfg = RenderConfig()
+    cam = s.device_camera
+    seq = [s.perturb(f) for f in range(4)]
+    ref = []
+    rd.upload(s)
+    for w, p, c in seq:
+        rd.update_params(w, p, c)
+        rd.render_frame(cam, cfg, exact=False, graph=True)
+        ref.append(rd.download_gbuffer())
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    ctxs = []
+    for st in streams:
+        r = Renderer(0)
+        r.set_stream(st.cuda_stream)
+        r.upload(s)
+        ctxs.append(r)
+    got = []
+    try:
+        for rnd in range(2):  # frames 0,1 concurrently, then 2,3
+            for k in range(2):
+                w, p, c = seq[2 * rnd + k]
+                ctxs[k].update_params(w, p, c)
+                ctxs[k].render_frame(cam, cfg, exact=False, graph=True)
+            torch.cuda.synchronize()
+            got += [ctxs[0].download_gbuffer(), ctxs[1].download_gbuffer()]
+    finally:
+        for r in ctxs:
+            r.close()
+    for a, b in zip(got, ref):
+        assert a.depth.tobytes() == b.depth.tobytes() and a.normal.tobytes() == b.normal.tobytes()
+        assert a.hit.tobytes() == b.hit.tobytes() and a.evalCount.tobytes() == b.evalCount.tobytes()
+
+
 def test_march_schedule_never_changes_results(rd):
     """Raster order, the device's longest-first order with half-tile units
     (mode 1) and a random host permutation give bit-identical frames and
