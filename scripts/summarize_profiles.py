@@ -93,7 +93,8 @@ def launches(path):
     for d in data:
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = d["Kernel Name"].split("(")[0].replace("btk::<unnamed>::", "").replace("void ", "")
+        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        name = name.replace("btk::<unnamed>::", "").replace("<unnamed>::", "").replace("btk::", "")
         agg[name][0] += 1
         scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[d["Metric Unit"]]
         agg[name][1] += float(d["Metric Value"].replace(",", "")) * scale
@@ -114,12 +115,16 @@ def main():
     lp = os.path.join(OUT, f"{tag}_launches.csv")
     if os.path.exists(lp):
         agg = launches(lp)
-        total = sum(v[1] for v in agg.values())
+        # the bench's own measurement helpers (FP32 peak microbenchmark, L2
+        # flush) run in the same process but are not part of a frame
+        helper = lambda k: "k_ffma_peak" in k or "FillFunctor" in k  # noqa: E731
+        total = sum(v[1] for k, v in agg.items() if not helper(k))
         lines += ["Cold-cache, serialised per-launch times (`ncu --metrics gpu__time_duration.sum --clock-control none`);",
-                  "compare shares, not absolutes.", "",
+                  "compare shares, not absolutes. Shares are of the frame kernels only.", "",
                   "| kernel | launches | us/launch | share |", "|---|---|---|---|"]
         for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
-            lines.append(f"| `{k}` | {n} | {us / n:.1f} | {us / total * 100:.1f}% |")
+            share = "(bench helper, not in the frame)" if helper(k) else f"{us / total * 100:.1f}%"
+            lines.append(f"| `{k}` | {n} | {us / n:.1f} | {share} |")
     open(os.path.join(PROF, f"{rnd}_{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
     traffic = {}
     for rep in sorted(f for f in os.listdir(OUT) if f.startswith(tag + "_prof_") and f.endswith(".ncu-rep")):
