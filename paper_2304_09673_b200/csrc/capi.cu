@@ -80,6 +80,10 @@ struct bt_ctx {
     int smClockKHz = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    // a captured frame forks independent stages onto `side` (camera || ROI + VOIs,
+    // march ordering || view build) and joins them back
+    cudaStream_t side = nullptr;
+    cudaEvent_t evFork[2] = {}, evJoin[2] = {};
 
     // tree
     DevBuf<float4> words;
@@ -384,16 +388,26 @@ int check_config(const bt_render_config* cfg) {
 // Rays, tile cones and pyramids for the superblock rows that meet
 // [tile0, tile1) (tile1 == 0: the whole image).  A sharded rank that does not
 // compute normals needs only its own rows.
-int do_camera(bt_ctx* c, const bt_camera& cam, uint32_t tile0 = 0, uint32_t tile1 = 0) {
+int do_camera(bt_ctx* c, const bt_camera& cam, uint32_t tile0 = 0, uint32_t tile1 = 0, cudaStream_t st = nullptr) {
     int rc = ensure_image(c, cam);
     if (rc) return rc;
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     if (tile1 == 0 || tile1 > tiles) tile1 = tiles;
     if (tile0 > tile1) tile0 = tile1;
-    launch_camera(c->stream, to_cam(cam), frame_bufs(c), c->tilesX, c->tilesY, tile0, tile1);
+    launch_camera(st ? st : c->stream, to_cam(cam), frame_bufs(c), c->tilesX, c->tilesY, tile0, tile1);
     c->haveRays = true;
     c->rayCam = cam;
     c->rayT1 = camera_tile_cover(c->tilesX, c->tilesY, tile0, tile1, &c->rayT0);
+    return BT_OK;
+}
+
+int ensure_side(bt_ctx* c) {
+    if (c->side) return BT_OK;
+    BT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        BT_CUDA(cudaEventCreateWithFlags(&c->evFork[i], cudaEventDisableTiming));
+        BT_CUDA(cudaEventCreateWithFlags(&c->evJoin[i], cudaEventDisableTiming));
+    }
     return BT_OK;
 }
 
@@ -475,9 +489,20 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
-    if (c->schedMode == 1)  // longest-first march units from the count pass's cost proxy
-        launch_tile_order(c->stream, view_bufs(c), trace_gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
-                          trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
+    // longest-first march units from the count pass's cost proxy; in a captured
+    // frame they are ordered on the side stream while the views are built
+    const bool forkOrder = c->schedMode == 1 && !checked;
+    if (forkOrder) {
+        int rc = ensure_side(c);
+        if (rc) return rc;
+        BT_CUDA(cudaEventRecord(c->evFork[1], c->stream));
+        BT_CUDA(cudaStreamWaitEvent(c->side, c->evFork[1], 0));
+    }
+    if (c->schedMode == 1)
+        launch_tile_order(forkOrder ? c->side : c->stream, view_bufs(c), trace_gbuf(c), c->orderHist.ptr,
+                          c->tileOrder.ptr, tile0, tile1, trace_grid_warps(c->smCount), split_beta(),
+                          2u * trace_grid_warps(c->smCount));
+    if (forkOrder) BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
     if (checked) {
         uint2 total{0u, 0u};
@@ -494,6 +519,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
     if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
+    if (forkOrder) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[1], 0));
     ViewBufs vbm = view_bufs(c);
     if (c->schedMode == 1) {
         vbm.order = c->tileOrder.ptr;
@@ -636,6 +662,14 @@ int bt_ctx_destroy(bt_ctx* c) {
             cudaEventDestroy(c->evCopied[i]);
             cudaEventDestroy(c->evCopied2[i]);
             c->snap[i].release();
+        }
+    }
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(c->evFork[i]);
+            cudaEventDestroy(c->evJoin[i]);
         }
     }
     cudaStreamDestroy(c->own);
@@ -1090,12 +1124,24 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
     if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
     const int mode = cfg->normalsMode;
     auto enqueue = [&](bool checked) -> int {
+        // normals need every ray of the image (they run over the assembled frame)
+        const uint32_t c0 = normals ? 0u : tile0, c1 = normals ? 0u : tile1;
+        int r = BT_OK;
+        if (!checked) {  // captured frame: the camera pass runs beside ROI + VOIs
+            r = ensure_side(c);
+            if (r) return r;
+            BT_CUDA(cudaEventRecord(c->evFork[0], c->stream));
+            BT_CUDA(cudaStreamWaitEvent(c->side, c->evFork[0], 0));
+            r = do_camera(c, *cam, c0, c1, c->side);
+            if (r) return r;
+            BT_CUDA(cudaEventRecord(c->evJoin[0], c->side));
+        }
         launch_roi_all(c->stream, dev_tree(c), c->roi.ptr);
         launch_voi(c->stream, dev_tree(c), c->roi.ptr, cfg->hitEpsilon, c->vois.ptr);
         c->haveRoi = true;
         c->nvoi = c->nprims;
-        // normals need every ray of the image (they run over the assembled frame)
-        int r = normals ? do_camera(c, *cam) : do_camera(c, *cam, tile0, tile1);
+        if (checked) r = do_camera(c, *cam, c0, c1);
+        else BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[0], 0));
         if (r) return r;
         r = do_abuffer(c, *cam, tile0, tile1, checked);
         if (r) return r;
