@@ -126,7 +126,7 @@ void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int til
 uint32_t camera_tile_cover(int tilesX, int tilesY, uint32_t tile0, uint32_t tile1, uint32_t* cover0);
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
                     const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
-                    int smCount);
+                    int smCount, bool zero = true);
 void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
 
 // ---- launchers (k_util.cu) -------------------------------------------
@@ -141,8 +141,10 @@ void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWor
 // ---- launchers (k_views.cu) -------------------------------------------
 // build=false: count pass + scan (the host may then read the totals and grow
 // the record buffers); build=true: write the interval/view records.
+// zero = false (every launcher): the frame's counters were already zeroed at
+// the start of a captured frame, off the critical path.
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
-                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build);
+                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build, bool zero = true);
 uint32_t view_scan_blocks(uint32_t tiles);
 size_t view_slab_words(uint32_t tiles);
 // longest-first march units of [tile0, tile1) from vb.tileCost (hist: 258 words of
@@ -155,14 +157,14 @@ uint32_t trace_grid_warps(int smCount);
 // ---- launchers (k_trace.cu) -------------------------------------------
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
-                  uint32_t tile1, int smCount, uint32_t* tileQueue);
+                  uint32_t tile1, int smCount, uint32_t* tileQueue, bool zero = true);
 // vb: the interval records of the march that produced this G-buffer (whole
 // frame, FMA path) -- the gradient fallback then evaluates the pruned view
 // of the interval each ray hit in; nullptr: the full tree (reference)
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
-                    const ViewBufs* vb);
+                    const ViewBufs* vb, bool zero = true);
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                    const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats);
 

@@ -84,6 +84,7 @@ struct bt_ctx {
     // march ordering || view build) and joins them back
     cudaStream_t side = nullptr;
     cudaEvent_t evFork[2] = {}, evJoin[2] = {};
+    bool prezeroed = false;  // enqueueing a captured frame whose counters were zeroed on `side`
 
     // tree
     DevBuf<float4> words;
@@ -433,7 +434,7 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
     }
     for (int attempt = 0; attempt < 8; ++attempt) {
         launch_abuffer(c->stream, to_cam(cam), c->vois.ptr, c->nvoi, frame_bufs(c), c->tilesX, c->tilesY,
-                       tile0, tile1, c->smCount);
+                       tile0, tile1, c->smCount, !c->prezeroed);
         if (!checked) break;
         uint32_t cnt[kCntSlots];
         BT_CUDA(cudaMemcpyAsync(cnt, c->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
@@ -488,7 +489,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const Cam k = to_cam(cam);
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
-    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false, !c->prezeroed);
     // longest-first march units from the count pass's cost proxy; in a captured
     // frame they are ordered on the side stream while the views are built
     const bool forkOrder = c->schedMode == 1 && !checked;
@@ -529,7 +530,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         vbm.unitCount = c->hostUnits.ptr;
     }
     launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, trace_gbuf(c), c->stats.ptr, tile0, tile1,
-                 c->smCount, c->tileQueue.ptr);
+                 c->smCount, c->tileQueue.ptr, !c->prezeroed);
     if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
         cudaEventSynchronize(c->ev[1]);
@@ -566,7 +567,7 @@ int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
     const ViewBufs vb = view_bufs(c);
     launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
                    c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps,
-                   c->viewsFrame && !exact ? &vb : nullptr);
+                   c->viewsFrame && !exact ? &vb : nullptr, !c->prezeroed);
     return BT_OK;
 }
 
@@ -1124,6 +1125,10 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
     if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
     const int mode = cfg->normalsMode;
     auto enqueue = [&](bool checked) -> int {
+        struct Reset {
+            bool& f;
+            ~Reset() { f = false; }
+        } reset{c->prezeroed};
         // normals need every ray of the image (they run over the assembled frame)
         const uint32_t c0 = normals ? 0u : tile0, c1 = normals ? 0u : tile1;
         int r = BT_OK;
@@ -1134,7 +1139,16 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
             BT_CUDA(cudaStreamWaitEvent(c->side, c->evFork[0], 0));
             r = do_camera(c, *cam, c0, c1, c->side);
             if (r) return r;
+            // the frame's counters and per-tile cursors, zeroed here instead of
+            // in front of each stage
+            const size_t tiles = (size_t)c->tilesX * c->tilesY;
+            BT_CUDA(cudaMemsetAsync(c->counters.ptr, 0, kCntSlots * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->tileCount.ptr, 0, tiles * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->tileCursor.ptr, 0, tiles * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->vCounters.ptr, 0, 2 * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->tileQueue.ptr, 0, sizeof(uint32_t), c->side));
             BT_CUDA(cudaEventRecord(c->evJoin[0], c->side));
+            c->prezeroed = true;
         }
         launch_roi_all(c->stream, dev_tree(c), c->roi.ptr);
         launch_voi(c->stream, dev_tree(c), c->roi.ptr, cfg->hitEpsilon, c->vois.ptr);

@@ -665,11 +665,13 @@ void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int til
 
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
                     const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
-                    int smCount) {
+                    int smCount, bool zero) {
     const uint32_t tiles = (uint32_t)(tilesX * tilesY);
-    cudaMemsetAsync(fb.counters, 0, kCntSlots * sizeof(uint32_t), st);
-    cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
-    cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
+    if (zero) {
+        cudaMemsetAsync(fb.counters, 0, kCntSlots * sizeof(uint32_t), st);
+        cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
+        cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
+    }
     if (nvoi > 0) {
         int sbLo, sbHi;
         sb_range(tilesX, tilesY, tile0, tile1, sbLo, sbHi);

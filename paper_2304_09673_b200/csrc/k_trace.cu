@@ -748,12 +748,12 @@ uint32_t trace_grid_warps(int smCount) { return trace_grid_blocks(smCount) * kTr
 
 void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam, const TraceParams& tp,
                   const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, uint64_t* stats, uint32_t tile0,
-                  uint32_t tile1, int smCount, uint32_t* tileQueue) {
+                  uint32_t tile1, int smCount, uint32_t* tileQueue, bool zero) {
     if (tile1 <= tile0) return;
     const size_t smem = sizeof(MarchSmem) * kTraceWarps;
     const uint32_t blocks =
         std::min<uint32_t>(trace_grid_blocks(smCount), (tile1 - tile0 + kTraceWarps - 1) / kTraceWarps);
-    cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
+    if (zero) cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
     void* args[] = {(void*)&t,    (void*)&cam,   (void*)&tp,    (void*)&fb,          (void*)&vb,       (void*)&g,
                     (void*)&stats, (void*)&tile0, (void*)&tile1, (void*)&tileQueue};
     cudaLaunchKernel(trace_fn(exact), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
@@ -762,9 +762,11 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
-                    const ViewBufs* vb) {
-    cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
-    cudaMemsetAsync(counters + kCntFallbackHard, 0, sizeof(uint32_t), st);
+                    const ViewBufs* vb, bool zero) {
+    if (zero) {
+        cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
+        cudaMemsetAsync(counters + kCntFallbackHard, 0, sizeof(uint32_t), st);
+    }
     dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
     k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
     const size_t bytes = (size_t)t.nFrontier * 6 * sizeof(float) + (size_t)t.nUpper * sizeof(uint32_t);

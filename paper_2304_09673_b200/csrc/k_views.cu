@@ -351,9 +351,9 @@ void launch_tile_order(cudaStream_t st, const ViewBufs& vb, const GBuf& g, uint3
 }
 
 void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
-                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build) {
+                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build, bool zero) {
     if (!build) {
-        cudaMemsetAsync(vb.counters, 0, 2 * sizeof(uint32_t), st);
+        if (zero) cudaMemsetAsync(vb.counters, 0, 2 * sizeof(uint32_t), st);
         k_view_count<<<(tiles + kViewWarps - 1) / kViewWarps, kViewWarps * 32, 0, st>>>(cam, tp, fb, vb, tile0,
                                                                                          tile1, tiles);
         const uint32_t nblocks = (tiles + kViewScanBlock - 1) / kViewScanBlock;
