@@ -177,16 +177,24 @@ __global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tiles
     __shared__ float4 sCone[64];
     __shared__ float sSin[64];
     __shared__ int sValid[64];
+    __shared__ float sScreen[2][kSB * kTile];  // screen offsets of the block's 64 columns and 64 rows
     const int sbX = (tilesX + kSB - 1) / kSB;
     const int sb = sb0 + (int)blockIdx.x;
     const int sx = sb % sbX, sy = sb / sbX;
+    if (threadIdx.x < 2 * kSB * kTile) {
+        const int j = threadIdx.x & (kSB * kTile - 1);
+        sScreen[threadIdx.x >> 6][j] = threadIdx.x < kSB * kTile
+                                           ? screen_x(cam, E::add((float)(sx * kSB * kTile + j), 0.5f))
+                                           : screen_y(cam, E::add((float)(sy * kSB * kTile + j), 0.5f));
+    }
+    __syncthreads();
     for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
         const int lt = k >> 6, pix = k & 63;
         const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
         if (tx >= tilesX || ty >= tilesY) continue;
         const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
         if (px >= cam.width || py >= cam.height) continue;
-        const RayDir r = pixel_ray(cam, px, py);
+        const RayDir r = ray_from_screen(cam, sScreen[0][px - sx * kSB * kTile], sScreen[1][py - sy * kSB * kTile]);
         fb.rays[(size_t)(ty * tilesX + tx) * 64 + pix] = make_float4(r.dir.x, r.dir.y, r.dir.z, r.ddf);
     }
     if (threadIdx.x < 64) {
