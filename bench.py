@@ -247,6 +247,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                 gather_rows(planes, rows, rank, world, W, H)
             if rank == 0:  # normals over the whole image (they need neighbour rows)
                 rd.compute_normals(cam, cfg.normalsMode, exact)
+            if fused:  # rank 0 has read every row: the next frame's peer writes may land
+                dist.all_reduce(done)
 
     for f in range(args.warmup):
         step(f)
@@ -281,6 +283,10 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     launches = args.steps * (kernels.value + 1)  # graph kernels + the parameter-update kernel
     value = W * H / (ms * 1e-3) / 1e6
 
+    e2e_multi = None
+    if world > 1:
+        e2e_multi = e2e_pass_multi(rd, scene, cam, cfg, exact, host_frames, args, rank, world, tile0, tile1, fused,
+                                   planes, rows)
     if rank != 0:
         return
     result = {
@@ -344,6 +350,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # ------------------------------------------------------------------ e2e through the C-ABI with host buffers
     if world == 1:
         result["e2e"] = e2e_pass(rd, scene, cam, cfg, exact, host_frames, args)
+    elif e2e_multi is not None:
+        result["e2e"] = e2e_multi
 
     # ------------------------------------------------------------------ CPU reference beside it
     if world == 1 and not args.no_cpu_baseline:
@@ -467,6 +475,76 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
                     "copy stream; frame N's D2H overlaps frame N+1's render), wall clock",
             "sync_variant": {"value": round(W * H / dt_sync / 1e6, 2), "ms_per_step": round(dt_sync * 1e3, 4),
                              "path": "same with the blocking bt_gbuffer_download per frame"}}
+
+
+def e2e_pass_multi(rd, scene, cam, cfg, exact, host_frames, args, rank, world, tile0, tile1, fused, planes,
+                   rows) -> dict | None:
+    """N GPUs end to end, wall clock, max over ranks: per step every rank
+    uploads the frame's parameter deltas from pinned host memory and traces
+    its tile rows into rank 0's G-buffer (fused gather, or the NCCL gather);
+    rank 0 computes the normals and streams the whole G-buffer into a pinned
+    host slab; every frame is on the host when the timed region ends."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_09673_b200 import _capi as capi
+    from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes
+    lib = rd.lib
+    dev = torch.device("cuda", torch.cuda.current_device())
+    W, H = scene.width, scene.height
+    n = len(scene.prims)
+    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    frames = [(pin(w.view(np.int32)), pin(p), pin(c.view(np.int32))) for w, p, c in host_frames]
+    slabs = []
+    if rank == 0:
+        off = (C.c_size_t * 7)()
+        total = C.c_size_t()
+        capi.check(lib.bt_gbuffer_layout(rd.ctx, off, C.byref(total)), "bt_gbuffer_layout")
+        slabs = [torch.empty(total.value, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    done = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step(f, i):
+        w, p, c = frames[f]
+        capi.check(lib.bt_params_update(rd.ctx, C.c_void_p(w.data_ptr()), C.c_void_p(p.data_ptr()),
+                                        C.c_void_p(c.data_ptr()), n, 17), "bt_params_update")
+        rd.render_frame(cam, cfg, exact=exact, graph=True, tile0=tile0, tile1=tile1, normals=False)
+        if fused:
+            dist.all_reduce(done)
+        else:
+            if not planes:
+                planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
+            gather_rows(planes, rows, rank, world, W, H)
+        if rank == 0:
+            rd.compute_normals(cam, cfg.normalsMode, exact)
+            capi.check(lib.bt_gbuffer_download_async_slab(rd.ctx, C.c_void_p(slabs[i % 2].data_ptr())),
+                       "bt_gbuffer_download_async_slab")
+        if fused:  # the snapshot is taken: the next frame's peer writes may land
+            dist.all_reduce(done)
+
+    for i in range(args.warmup):
+        step(i, i)
+    if rank == 0:
+        capi.check(lib.bt_download_wait(rd.ctx), "bt_download_wait")
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i, i)
+    if rank == 0:
+        capi.check(lib.bt_download_wait(rd.ctx), "bt_download_wait")
+    torch.cuda.synchronize(dev)
+    dt = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dt = float(dt.item())
+    tx, ty = scene.tiles
+    return {"value": round(W * H / dt / 1e6, 2), "unit": "Mrays/s", "ms_per_step": round(dt * 1e3, 4),
+            "h2d_bytes_per_step": world * n * (4 + 17 * 4 + 4),
+            "d2h_bytes_per_step": W * H * (1 + 4 + 12 + 4) + tx * ty * (4 + 4 + 1),
+            "path": "every rank: bt_params_update (pinned host) -> bt_render_frame (its tile rows, "
+                    f"{'fused gather into rank 0' if fused else 'NCCL gather to rank 0'}); rank 0: bt_normals -> "
+                    "bt_gbuffer_download_async_slab (pinned host); wall clock, max over ranks"}
 
 
 def eager_stages(r, cam, cfg, exact, frames: int = 3) -> dict:
