@@ -75,14 +75,15 @@ __global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TracePa
             }
             if (lane == 0) slab[0] = fits ? c.x : kSlabOverflow;
         }
-        // march cost proxy for longest-first scheduling: fragment count plus
-        // the summed NDC depth extent of the tile's fragments
+        // march cost proxy for longest-first scheduling: 2 x fragments + the
+        // view-node bound (c.y: sum of 2 nAct - 1 over the intervals) + 16 x
+        // the summed NDC depth extent of the fragments (scripts/proxy_ab.sh)
         float span = 0.0f;
         for (uint32_t i = lane; i < cnt; i += 32)
             span += __ldg(&fb.frags[off + i].zExit) - __ldg(&fb.frags[off + i].zEntry);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(kFull, span, o);
-        if (lane == 0) vb.tileCost[tile] = min(255u, 4u * cnt + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
+        if (lane == 0) vb.tileCost[tile] = min(255u, 2u * cnt + c.y + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
     }
     if (lane == 0) vb.count[tile] = c;
 }
