@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TracePa
     const uint32_t tile = blockIdx.x * kViewWarps + wid;
     if (tile >= tiles) return;
     uint2 c = make_uint2(0u, 0u);
+    float wsum = 0.0f;  // scheduling cost of the tile's views (below)
     if (tile >= tile0 && tile < tile1) {
         const uint32_t off = fb.offsets[tile];
         const uint32_t cnt = fb.offsets[tile + 1] - off;
@@ -72,18 +73,25 @@ __global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TracePa
                 }
                 c.x += 1u;
                 c.y += 2u * n - 1u;
+                {  // view-node bound weighted by the interval's length in view z (fetch windows)
+                    const float dvz = FastOps::rcp(cam.invNear - f.zEnd * FastOps::rcp(cam.invDepthRange)) -
+                                      FastOps::rcp(cam.invNear - zb * FastOps::rcp(cam.invDepthRange));
+                    const float rel = fmaxf(dvz, 0.0f) * FastOps::rcp(tp.window);
+                    wsum += (float)(2u * n - 1u) * fminf(4.0f, 1.0f + 4.0f * rel);
+                }
             }
             if (lane == 0) slab[0] = fits ? c.x : kSlabOverflow;
         }
         // march cost proxy for longest-first scheduling: 2 x fragments + the
-        // view-node bound (c.y: sum of 2 nAct - 1 over the intervals) + 16 x
-        // the summed NDC depth extent of the fragments (scripts/proxy_ab.sh)
+        // view-node bound (2 nAct - 1 per interval) weighted by the interval's
+        // view-z length in fetch windows (1x .. 4x) + 16 x the summed NDC depth
+        // extent of the fragments (variants compared with scripts/proxy_ab.sh)
         float span = 0.0f;
         for (uint32_t i = lane; i < cnt; i += 32)
             span += __ldg(&fb.frags[off + i].zExit) - __ldg(&fb.frags[off + i].zEntry);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(kFull, span, o);
-        if (lane == 0) vb.tileCost[tile] = min(255u, 2u * cnt + c.y + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
+        if (lane == 0) vb.tileCost[tile] = min(255u, 2u * cnt + (uint32_t)wsum + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
     }
     if (lane == 0) vb.count[tile] = c;
 }
