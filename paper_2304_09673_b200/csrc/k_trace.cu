@@ -591,6 +591,7 @@ constexpr int kGradViewWarps = 4;
 __global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t, Cam cam, FrameBufs fb, ViewBufs vb,
                                                                         GBuf g, uint32_t* counters, uint64_t* stats) {
     __shared__ uint32_t sh[kGradViewWarps][kViewCap], sw[kGradViewWarps][kViewCap];
+    __shared__ float4 blk[kGradViewWarps][kMarchBlocks];  // fast parameter blocks, as in k_march
     __shared__ float res[kGradViewWarps][6];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t n = counters[kCntFallback];
@@ -630,10 +631,14 @@ __global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t
         }
         const IntervalRec rec = vb.iv[o.x + (uint32_t)sel];
         const uint32_t nView = rec.viewPrim & 0xFFFFu;
+        // the view's parameter blocks are converted lane-parallel (one round of
+        // loads) instead of read node by node inside the evaluation
+        const bool fits = rec.nBlocks <= kMarchBlocks;
         for (uint32_t j = lane; j < nView; j += 32) {
             const uint2 nd = vb.nodes[rec.nodeOff + j];
             sh[w][j] = nd.x;
             sw[w][j] = nd.y;
+            if (fits) convert_node(nd.x, t.words + nd.y + 1, blk[w] + ((nd.x & 0xFFFFu) >> 4));
         }
         __syncwarp();
         const F3 pc = vadd<E>(cam.pos, vscale<E>(F3{r.x, r.y, r.z}, depth));
@@ -644,7 +649,10 @@ __global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t
             if (lane < 2) tap.x = E::add(pc.x, s);
             else if (lane < 4) tap.y = E::add(pc.y, s);
             else tap.z = E::add(pc.z, s);
-            res[w][lane] = eval_staged<FastOps>(sh[w], sw[w], nView, t.words, tap);
+            float v;
+            if (fits) eval_view_fast<1>(sh[w], nView, blk[w], &tap, &v);
+            else v = eval_staged<FastOps>(sh[w], sw[w], nView, t.words, tap);
+            res[w][lane] = v;
         }
         __syncwarp();
         if (lane == 0) {
