@@ -39,7 +39,10 @@ constexpr uint32_t kSlabOverflow = 0xFFFFFFFFu;
 // Warp per tile (WarpFetch): run the fetch sequence, count intervals and the
 // view-node bound, and keep the intervals in the tile's slab; lane 0 also
 // records the scheduling cost proxy.
-__global__ void __launch_bounds__(kViewWarps * 32) k_view_count(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
+#ifndef BT_VIEW_MINB
+#define BT_VIEW_MINB 8  // CTAs per SM the register budget must fit (scripts/viewminb_ab.sh)
+#endif
+__global__ void __launch_bounds__(kViewWarps * 32, BT_VIEW_MINB) k_view_count(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
                                                                 uint32_t tile0, uint32_t tile1, uint32_t tiles) {
     __shared__ WarpFetchSmem sm[kViewWarps];
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(1024) k_view_scan(ViewBufs vb, uint32_t tiles)
 // The words go to the LAST nAct slots of the interval's 2 nAct - 1 node
 // slots, so the in-place view build below never overwrites an active word
 // before reading it (after active i at most 2i + 1 nodes are written).
-__global__ void __launch_bounds__(kViewWarps * 32) k_view_fetch(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
+__global__ void __launch_bounds__(kViewWarps * 32, BT_VIEW_MINB) k_view_fetch(Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb,
                                                                 uint32_t tile0, uint32_t tile1) {
     __shared__ WarpFetchSmem sm[kViewWarps];
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
