@@ -171,9 +171,12 @@ __device__ __forceinline__ bool volume_pyramid_may_touch(const float4* pl, F3 ap
     return true;
 }
 
+#ifndef BT_RASTER_MINB
+#define BT_RASTER_MINB 4  // CTAs per SM of k_camera / k_raster the register budget must fit (scripts/rasterminb_ab.sh)
+#endif
 // One CTA per superblock: 4096 rays, 64 tile cones, 1 conservative
 // superblock cone containing all of its tile cones.
-__global__ void __launch_bounds__(256) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY, int sb0) {
+__global__ void __launch_bounds__(256, BT_RASTER_MINB) k_camera(Cam cam, FrameBufs fb, int tilesX, int tilesY, int sb0) {
     __shared__ float4 sCone[64];
     __shared__ float sSin[64];
     __shared__ int sValid[64];
@@ -412,7 +415,7 @@ constexpr uint32_t kNoFragment = 0xFFFFFFFFu;
 // clipped to [near, far], mapped to NDC and reduced with min/max (order-free
 // on these finite values).  The fragment lands in the item's own slot, so no
 // global append counter is contended; misses mark the slot empty.
-__global__ void __launch_bounds__(256) k_raster(Cam cam, const Voi* vois, FrameBufs fb) {
+__global__ void __launch_bounds__(256, BT_RASTER_MINB) k_raster(Cam cam, const Voi* vois, FrameBufs fb) {
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t nitems = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
