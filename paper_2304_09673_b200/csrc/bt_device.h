@@ -18,6 +18,11 @@ struct DevTree {
     const uint32_t* primOrd = nullptr;     // node ordinal of each primitive
     const uint32_t* nodeWord = nullptr;    // word of each node ordinal
     const int32_t* compactAnc = nullptr;   // nearest strict compact ancestor ordinal, -1 none
+    // every node's compact strict ancestors as a CSR list of their parameter
+    // words (ancOff[nnodes + 1], ancIdx): ROI loads them independently instead
+    // of walking the chain (deep trees); null when the lists would be too long
+    const uint32_t* ancOff = nullptr;
+    const uint32_t* ancIdx = nullptr;
     const uint32_t* fullProgram = nullptr; // post-order (isPrim<<31 | op<<26 | word)
     uint32_t nwords = 0, nnodes = 0, nprims = 0;
     uint32_t fullDepth = 0;                // max stack depth of a full post-order walk

@@ -92,6 +92,8 @@ struct bt_ctx {
     DevBuf<uint2> frontier;
     uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0, upperIsMinChain = 0;
     DevBuf<int32_t> compactAnc, parentOrd, fastScratch;
+    DevBuf<uint32_t> ancOff, ancIdx;  // compact-ancestor lists (k_roi_all)
+    bool haveAncLists = false;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
     uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
@@ -173,6 +175,8 @@ DevTree dev_tree(const bt_ctx* c) {
     t.primOrd = c->primOrd.ptr;
     t.nodeWord = c->nodeWord.ptr;
     t.compactAnc = c->compactAnc.ptr;
+    t.ancOff = c->haveAncLists ? c->ancOff.ptr : nullptr;
+    t.ancIdx = c->haveAncLists ? c->ancIdx.ptr : nullptr;
     t.fullProgram = c->fullProgram.ptr;
     t.nwords = c->nwords;
     t.nnodes = c->nnodes;
@@ -621,6 +625,8 @@ int bt_ctx_destroy(bt_ctx* c) {
         b->release();
     c->words.release();
     c->compactAnc.release();
+    c->ancOff.release();
+    c->ancIdx.release();
     c->parentOrd.release();
     c->fastScratch.release();
     c->roi.release();
@@ -731,6 +737,15 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
         const uint8_t op = nodes[p].nodeOp;
         compactAnc[i] = (op >= 9 && op <= 11) ? p : compactAnc[p];
     }
+    // the compact-ancestor chains as CSR lists of parameter words (capped:
+    // a very deep all-compact comb keeps the chain walk)
+    std::vector<uint32_t> ancOff(nnodes + 1, 0), ancIdx;
+    bool ancLists = true;
+    for (uint32_t i = 0; i < nnodes && ancLists; ++i) {
+        for (int32_t a = compactAnc[i]; a >= 0; a = compactAnc[a]) ancIdx.push_back(nodes[a].word + 1);
+        ancOff[i + 1] = (uint32_t)ancIdx.size();
+        if (ancIdx.size() > (size_t)(1u << 24)) ancLists = false;
+    }
     // map primitive words to ordinals (both ascending)
     {
         uint32_t k = 0;
@@ -810,6 +825,15 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->primOrd.ptr, primOrd.data(), nprims * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->nodeWord.ptr, nodeWord.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->compactAnc.ptr, compactAnc.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    c->haveAncLists = ancLists;
+    if (ancLists) {
+        BT_CUDA(c->ancOff.reserve(nnodes + 1));
+        BT_CUDA(c->ancIdx.reserve(std::max<size_t>(1, ancIdx.size())));
+        BT_CUDA(cudaMemcpyAsync(c->ancOff.ptr, ancOff.data(), (nnodes + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+        if (!ancIdx.empty())
+            BT_CUDA(cudaMemcpyAsync(c->ancIdx.ptr, ancIdx.data(), ancIdx.size() * 4, cudaMemcpyHostToDevice,
+                                    c->stream));
+    }
     BT_CUDA(cudaMemcpyAsync(c->parentOrd.ptr, parentOrd.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->fullProgram.ptr, program.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->frontier.ptr, frontier.data(), frontier.size() * sizeof(uint2), cudaMemcpyHostToDevice,

@@ -52,7 +52,17 @@ __device__ __forceinline__ float roi_of(const DevTree& t, uint32_t ord) {
 
 __global__ void k_roi_all(DevTree t, float* roi) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < t.nnodes) roi[i] = roi_of(t, i);
+    if (i >= t.nnodes) return;
+    if (!t.ancOff) {
+        roi[i] = roi_of(t, i);
+        return;
+    }
+    // the same maximum, over independent loads (max of finite values starting
+    // from +0 does not depend on the order)
+    float r = 0.0f;
+    const uint32_t k1 = t.ancOff[i + 1];
+    for (uint32_t k = t.ancOff[i]; k < k1; ++k) r = smax(r, __ldg(&t.words[t.ancIdx[k]].y));
+    roi[i] = r;
 }
 
 __global__ void k_voi(DevTree t, const float* roi, float margin, Voi* vois) {
