@@ -494,8 +494,22 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false, !c->prezeroed);
-    // longest-first march units from the count pass's cost proxy; in a captured
-    // frame they are ordered on the side stream while the views are built
+    if (checked) {  // the totals: grow the record buffers and recount if short
+        uint2 total{0u, 0u};
+        BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
+                                cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        if (total.x > c->vIv.cap || total.y > c->vNodes.cap) {
+            if (total.x > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)total.x * 2));
+            if (total.y > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)total.y * 2));
+            c->bufEpoch++;
+            launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+        }
+    }
+    // longest-first march units from the FINAL count pass's cost proxy (the
+    // ordering zeroes tileCost of split tiles: a recount after it would undo
+    // that); in a captured frame they are ordered on the side stream while the
+    // views are built
     const bool forkOrder = c->schedMode == 1 && !checked;
     if (forkOrder) {
         int rc = ensure_side(c);
@@ -509,18 +523,6 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
                           2u * trace_grid_warps(c->smCount));
     if (forkOrder) BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
-    if (checked) {
-        uint2 total{0u, 0u};
-        BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
-                                cudaMemcpyDeviceToHost, c->stream));
-        BT_CUDA(cudaStreamSynchronize(c->stream));
-        if (total.x > c->vIv.cap || total.y > c->vNodes.cap) {
-            if (total.x > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)total.x * 2));
-            if (total.y > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)total.y * 2));
-            c->bufEpoch++;
-            launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
-        }
-    }
     if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
     if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
