@@ -494,6 +494,15 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const TraceParams tp = trace_params(cfg, cam);
     if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false, !c->prezeroed);
+    // longest-first march units from the count pass's cost proxy; in a captured
+    // frame they are ordered on the side stream while the views are built
+    auto order = [&](cudaStream_t st) {
+        launch_tile_order(st, view_bufs(c), trace_gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
+                          trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
+    };
+    const bool forkOrder = c->schedMode == 1 && !checked;
+    if (c->schedMode == 1 && checked) order(c->stream);  // overlaps the host's readback below
+    if (c->profiling) cudaEventRecord(c->ev[3], c->stream);  // (the readback is not stage time)
     if (checked) {  // the totals: grow the record buffers and recount if short
         uint2 total{0u, 0u};
         BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
@@ -504,25 +513,19 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
             if (total.y > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)total.y * 2));
             c->bufEpoch++;
             launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
+            // the recount rewrote tileCost, which the ordering zeroes on split
+            // tiles (their once-only error count): order again
+            if (c->schedMode == 1) order(c->stream);
         }
     }
-    // longest-first march units from the FINAL count pass's cost proxy (the
-    // ordering zeroes tileCost of split tiles: a recount after it would undo
-    // that); in a captured frame they are ordered on the side stream while the
-    // views are built
-    const bool forkOrder = c->schedMode == 1 && !checked;
     if (forkOrder) {
         int rc = ensure_side(c);
         if (rc) return rc;
         BT_CUDA(cudaEventRecord(c->evFork[1], c->stream));
         BT_CUDA(cudaStreamWaitEvent(c->side, c->evFork[1], 0));
+        order(c->side);
+        BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     }
-    if (c->schedMode == 1)
-        launch_tile_order(forkOrder ? c->side : c->stream, view_bufs(c), trace_gbuf(c), c->orderHist.ptr,
-                          c->tileOrder.ptr, tile0, tile1, trace_grid_warps(c->smCount), split_beta(),
-                          2u * trace_grid_warps(c->smCount));
-    if (forkOrder) BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
-    if (c->profiling) cudaEventRecord(c->ev[3], c->stream);
     if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
     if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
