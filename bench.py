@@ -112,10 +112,44 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# ---------------------------------------------------------------------------- shared config
+
+CONFIG_SIZES = {"C1": (10, 512, 512), "C2": (142, 1920, 1080), "C3": (1000, 1920, 1080), "C4": (10000, 3840, 2160),
+                "C5": (4000, 1920, 1080)}
+
+
+def bench_config(config: str, arm: dict) -> dict:
+    """The `config` object of both arms: the same keys, the workload keys with
+    the same values; `arm` fills what differs by nature (field arithmetic,
+    L2 handling, parallelism)."""
+    prims, w, h = CONFIG_SIZES.get(config, (None, None, None))
+    out = {"workload": WORKLOAD if config == "C3" else config, "primitives": prims,
+           "resolution": f"{w}x{h}" if w else None, "rays_per_frame": w * h if w else None,
+           "field_eval": None, "l2": None, "parallelism": None, "graph": None}
+    out.update(arm)
+    return out
+
+
+def host_cpu() -> dict:
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
 # ---------------------------------------------------------------------------- reference arm
 
-def cpu_frame_reference(config: str, frames: int, threads: int):
-    """Time the unmodified reference library (oracle/_ref) on `frames` frames."""
+def cpu_frame_reference(config: str, frames: int, threads: int, median: bool = False):
+    """Time the unmodified reference library (oracle/_ref) on `frames`
+    perturbed frames.  Returns (rays, wall seconds per frame, per-stage ms:
+    the mean over all frames, or with median=True the median over all but the
+    first, warm-up frame)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bridge import RefScene, ref_available  # CPU checker: bench's CPU legs only
     from paper_2304_09673_b200.pipeline import RenderConfig
@@ -130,6 +164,8 @@ def cpu_frame_reference(config: str, frames: int, threads: int):
         _, _, ms, _ = r.frame(cfg, threads)
         times.append(time.perf_counter() - t0)
         stages.append(ms)
+    if median:
+        return r.width * r.height, times, np.median(np.asarray(stages[1:]), axis=0)
     return r.width * r.height, times, np.mean(stages, axis=0)
 
 
@@ -153,7 +189,12 @@ def run_reference(args, rank: int):
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.config == "C3" else args.config, "threads": threads},
+        "config": bench_config(args.config, {
+            "field_eval": "ieee (the reference's own CPU code, unmodified)",
+            "l2": "n/a (CPU path; each frame re-reads the whole scene from host memory)",
+            "parallelism": f"{threads} host threads (render_tiles, oracle_render); rasterize_volumes single-threaded",
+            "graph": "n/a"}),
+        "host_cpu": host_cpu(),
         "cpu_baseline": {"value": round(value, 3), "unit": "Mrays/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -256,6 +297,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
 
     # ------------------------------------------------------------------ timed region
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    rd.reset_stats()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -273,6 +315,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         t_wall = time.perf_counter() - t_wall
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
+    # a graph replay that outgrew a capacity only flags it (the frame is
+    # emptied, never written out of bounds): bt_stats_download raises
+    # BT_ENOMEM then, and a flagged frame must not be reported as a speed
+    st_timed = rd.stats()
+    assert st_timed.tileErrors == 0, f"{st_timed.tileErrors} tile errors in the timed frames"
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -293,14 +340,13 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": round(value, 2), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural scene, fixed seed)",
-        "config": {"workload": WORKLOAD if args.config == "C3" else args.config, "primitives": nprim,
-                   "resolution": f"{W}x{H}", "rays_per_frame": W * H,
-                   "field_eval": "ieee-exact" if exact else "fma-contracted (tolerance path)",
-                   "l2": "flushed between timed frames (256 MiB device write, untimed)",
-                   "parallelism": (f"tile rows over {world} GPU(s), "
-                                   f"{'fused gather (IPC peer writes)' if fused else 'NCCL gather'}")
-                                  if world > 1 else "1 GPU",
-                   "graph": f"{kernels.value} kernels / {nodes.value} nodes per frame"},
+        "config": bench_config(args.config, {
+            "field_eval": "ieee-exact" if exact else "fma-contracted (tolerance path)",
+            "l2": "flushed between timed frames (256 MiB device write, untimed)",
+            "parallelism": (f"tile rows over {world} GPU(s), "
+                            f"{'fused gather (IPC peer writes)' if fused else 'NCCL gather'}")
+                           if world > 1 else "1 GPU",
+            "graph": f"{kernels.value} kernels / {nodes.value} nodes per frame"}),
         "gpu_launches": launches,
         "clocks": {k: clock[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
     }
@@ -356,15 +402,20 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # ------------------------------------------------------------------ CPU reference beside it
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        out = cpu_frame_reference(args.config, 1, threads)
+        out = cpu_frame_reference(args.config, 6, threads, median=True)
         if out is not None:
             rays, times, stages = out
-            v = rays / times[0] / 1e6
+            med = float(np.median(times[1:]))
+            v = rays / med / 1e6
+            names = ("roi_voi", "rasterize_volumes", "render_tiles", "compute_normals")
             result["cpu_baseline"] = {
                 "value": round(v, 3), "unit": "Mrays/s", "cores": threads, "kind": "reference",
-                "sample": f"1 full {args.config} frame through the unmodified reference (oracle/_ref): stage ms "
-                          f"roi+voi {stages[0]:.1f}, rasterize {stages[1]:.1f} (single-threaded by design), "
-                          f"render_tiles {stages[2]:.1f} ({threads} threads), normals {stages[3]:.1f}"}
+                "host_cpu": host_cpu(), "ms_per_frame": round(med * 1e3, 2),
+                "stages_ms_median": {n: round(float(x), 2) for n, x in zip(names, stages)},
+                "sample": f"6 perturbed {args.config} frames through the unmodified reference (oracle/_ref), the "
+                          f"first a warm-up, per-stage median of the other 5: rasterize_volumes single-threaded by "
+                          f"design, render_tiles and compute_normals on {threads} threads; the reference's "
+                          f"steady_clock stage timers"}
     if not args.no_sweep and world == 1:
         result["sweep_ms_per_frame"] = sweep(rd, exact)
         result["frames_in_flight"] = frames_in_flight(scene, cam, cfg, exact, d_words, d_params, d_counts, nprim)
@@ -627,7 +678,7 @@ def sweep(rd_unused, exact) -> dict:
     cfg = RenderConfig()
     stream = torch.cuda.current_stream()
     assert stream.cuda_stream != 0
-    for name in ("C1", "C2", "C5"):
+    for name in ("C1", "C2", "C5", "C4"):
         s = Scene.build(name)
         r = Renderer(torch.cuda.current_device())
         r.set_stream(stream.cuda_stream)

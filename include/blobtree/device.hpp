@@ -8,6 +8,7 @@
 // the whole chain (a) -> (b) -> (c) -> normals replays from one CUDA graph.
 #pragma once
 
+#include <mutex>
 #include <vector>
 
 #include "../bt_cuda.h"
@@ -54,7 +55,22 @@ private:
     std::vector<float> stagedParams_;
 };
 
-// process-wide context used by the free functions of the drop-in API
+// process-wide context used by the free functions of the drop-in API.  A
+// bt_ctx is not thread-safe, while the reference's free functions are
+// reentrant: each drop-in call holds a ContextLease for its whole
+// upload -> launch -> download sequence, so calls from several host threads
+// serialise instead of interleaving on the shared context.
 bt_ctx* default_context();
+
+class ContextLease {
+public:
+    ContextLease();
+    operator bt_ctx*() const { return ctx_; }
+    bt_ctx* get() const { return ctx_; }
+
+private:
+    std::unique_lock<std::mutex> lock_;
+    bt_ctx* ctx_;
+};
 
 }  // namespace blobtree

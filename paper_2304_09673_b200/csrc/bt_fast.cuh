@@ -136,7 +136,7 @@ BT_DEV float f_quadric(float4 e, float4 g, float4 h, F3 l) {  // f0 / max(|grad 
 // One primitive at NP points; the parameter block is loaded once.
 template <int NP>
 BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v) {
-    if (kind == 0u) {
+    if (kind == 0u) {  // sqrt(x) - r of a finite point: never NaN (no filter needed)
         const float4 c = B[0];
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_sphere(c, p[i]);
@@ -165,8 +165,12 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_quadric(e, g, h, l[i]);
     }
-    // no NaN filter needed here: with finite points and validated parameters
-    // none of these closed forms produces NaN (the reference filters to 0)
+    // the reference's NaN -> 0 filter (field.cpp:283).  Validated parameters
+    // and finite points never produce NaN in these closed forms, but trees
+    // uploaded straight through the C-ABI are not validated: keep the filter
+    // (one FSETP + FSEL per primitive value).
+#pragma unroll
+    for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(v[i]);
 }
 
 // Operators on the fast path.  FMNMX-based min/max (fminf/fmaxf) instead of

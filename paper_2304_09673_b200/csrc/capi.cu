@@ -33,6 +33,15 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+// launch errors (bad configuration, missing attribute, ...) of the kernels
+// just enqueued; checked at the end of every eager entry point
+int launch_status() {
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return 0;
+    g_lastError = std::string("kernel launch: ") + cudaGetErrorString(e);
+    return BT_ECUDA;
+}
+
 #define BT_CUDA(call)                                                                    \
     do {                                                                                 \
         cudaError_t e_ = (call);                                                         \
@@ -99,6 +108,10 @@ struct bt_ctx {
     uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
     bool haveTree = false;
     bool haveRoi = false;
+    // host copy of the uploaded structure: a re-upload of the same structure
+    // (the drop-in free functions upload on every call) only copies the words
+    std::vector<bt_node> hostNodes;
+    std::vector<uint32_t> hostPrimWords;
 
     // parameter staging
     DevBuf<uint32_t> pWords, pCounts;
@@ -167,6 +180,24 @@ struct bt_ctx {
 };
 
 namespace {
+
+// Every entry point runs on its context's device: a process may hold
+// contexts on several GPUs, and the caller's thread may have any device
+// current.  The previous device is restored on return.
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(const bt_ctx* c) {
+        if (!c) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess)
+            prev = cur;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard&) = delete;
+    DevGuard& operator=(const DevGuard&) = delete;
+};
 
 DevTree dev_tree(const bt_ctx* c) {
     DevTree t;
@@ -492,7 +523,10 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const DevTree t = dev_tree(c);
     const Cam k = to_cam(cam);
     const TraceParams tp = trace_params(cfg, cam);
-    if (c->profiling) cudaEventRecord(c->ev[2], c->stream);
+    // stage events only in eager frames: synchronising on an event inside a
+    // stream capture would invalidate the capture
+    const bool prof = c->profiling && checked;
+    if (prof) cudaEventRecord(c->ev[2], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false, !c->prezeroed);
     // longest-first march units from the count pass's cost proxy; in a captured
     // frame they are ordered on the side stream while the views are built
@@ -502,7 +536,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     };
     const bool forkOrder = c->schedMode == 1 && !checked;
     if (c->schedMode == 1 && checked) order(c->stream);  // overlaps the host's readback below
-    if (c->profiling) cudaEventRecord(c->ev[3], c->stream);  // (the readback is not stage time)
+    if (prof) cudaEventRecord(c->ev[3], c->stream);  // (the readback is not stage time)
     if (checked) {  // the totals: grow the record buffers and recount if short
         uint2 total{0u, 0u};
         BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
@@ -526,9 +560,9 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         order(c->side);
         BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     }
-    if (c->profiling) cudaEventRecord(c->ev[4], c->stream);
+    if (prof) cudaEventRecord(c->ev[4], c->stream);
     launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
-    if (c->profiling) cudaEventRecord(c->ev[5], c->stream);
+    if (prof) cudaEventRecord(c->ev[5], c->stream);
     if (forkOrder) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[1], 0));
     ViewBufs vbm = view_bufs(c);
     if (c->schedMode == 1) {
@@ -540,7 +574,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     }
     launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, trace_gbuf(c), c->stats.ptr, tile0, tile1,
                  c->smCount, c->tileQueue.ptr, !c->prezeroed);
-    if (c->profiling) {  // sub-stage split: views (count+scan, build) and the march alone
+    if (prof) {  // sub-stage split: views (count+scan, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
         cudaEventSynchronize(c->ev[1]);
         float a = 0.f, b = 0.f, m = 0.f;
@@ -619,6 +653,7 @@ int bt_ctx_create(int device, bt_ctx** out) {
 }
 
 int bt_ctx_destroy(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return BT_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
@@ -690,6 +725,7 @@ int bt_ctx_destroy(bt_ctx* c) {
 }
 
 int bt_sync(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     BT_CUDA(cudaStreamSynchronize(c->stream));
     if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
@@ -699,6 +735,7 @@ int bt_sync(bt_ctx* c) {
 }
 
 int bt_set_stream(bt_ctx* c, void* s) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     c->stream = s ? (cudaStream_t)s : c->own;
     c->haveGraph = false;
@@ -706,6 +743,7 @@ int bt_set_stream(bt_ctx* c, void* s) {
 }
 
 int bt_device_info(bt_ctx* c, int* sm, int* clk) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (sm) *sm = c->smCount;
     if (clk) *clk = c->smClockKHz;
@@ -714,10 +752,27 @@ int bt_device_info(bt_ctx* c, int* sm, int* clk) {
 
 int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node* nodes, uint32_t nnodes,
                    const uint32_t* primitiveWords, uint32_t nprims, uint32_t rootWord) {
+    DevGuard dg_(c);
     if (!c || !data || !nodes || !primitiveWords) return fail(BT_EINVAL, "null tree buffer");
     if (nwords == 0 || nnodes == 0 || nprims == 0) return fail(BT_EINVAL, "empty tree");
     if (nwords >= BT_ANCESTOR_SENTINEL) return fail(BT_EINVAL, "tree exceeds the 23-bit node index space");
     (void)rootWord;
+    // frame products of the previous tree must not be marched or shaded
+    // against the new one (fragment words, view nodes index its words)
+    c->haveAbuffer = false;
+    c->haveGbuffer = false;
+    c->viewsFrame = false;
+    if (c->haveTree && nwords == c->nwords && nnodes == c->nnodes && nprims == c->nprims &&
+        std::memcmp(c->hostNodes.data(), nodes, (size_t)nnodes * sizeof(bt_node)) == 0 &&
+        std::memcmp(c->hostPrimWords.data(), primitiveWords, (size_t)nprims * 4) == 0) {
+        // same structure: the side tables stay valid, only parameters changed
+        BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        c->haveRoi = false;
+        c->nvoi = 0;
+        return BT_OK;
+    }
+    c->haveTree = false;
     // structure-only side tables
     std::vector<uint32_t> nodeWord(nnodes), primOrd(nprims), program(nnodes);
     std::vector<int32_t> parentOrd(nnodes, -1), compactAnc(nnodes, -1);
@@ -855,6 +910,8 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     c->nvoi = 0;
     c->fullDepth = maxd;
     c->gradWarps = 0;  // re-sized for the new primitive count on first use
+    c->hostNodes.assign(nodes, nodes + nnodes);
+    c->hostPrimWords.assign(primitiveWords, primitiveWords + nprims);
     c->haveTree = true;
     c->haveRoi = false;
     c->bufEpoch++;
@@ -862,6 +919,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
 }
 
 int bt_tree_download(bt_ctx* c, float* data, uint32_t nwords) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     if (nwords > c->nwords) return fail(BT_EINVAL, "nwords exceeds the uploaded tree");
     BT_CUDA(cudaMemcpyAsync(data, c->words.ptr, (size_t)nwords * 16, cudaMemcpyDeviceToHost, c->stream));
@@ -870,6 +928,7 @@ int bt_tree_download(bt_ctx* c, float* data, uint32_t nwords) {
 }
 
 int bt_tree_fast_indices(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     BT_CUDA(c->fastScratch.reserve((size_t)c->nnodes * 4));
     launch_fast_indices(c->stream, c->words.ptr, c->nodeWord.ptr, c->parentOrd.ptr, c->nnodes, c->fastScratch.ptr);
@@ -879,6 +938,7 @@ int bt_tree_fast_indices(bt_ctx* c) {
 
 int bt_params_update_device(bt_ctx* c, const uint32_t* dw, const float* dp, const uint32_t* dc, uint32_t n,
                             uint32_t stride) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     if (n == 0) return BT_OK;
     launch_params_update(c->stream, c->words.ptr, dw, dp, dc, n, stride);
@@ -887,6 +947,7 @@ int bt_params_update_device(bt_ctx* c, const uint32_t* dw, const float* dp, cons
 
 int bt_params_update(bt_ctx* c, const uint32_t* words, const float* params, const uint32_t* counts, uint32_t n,
                      uint32_t stride) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     if (n == 0) return BT_OK;
     if (!words || !params || !counts) return fail(BT_EINVAL, "null parameter buffer");
@@ -928,6 +989,7 @@ int bt_params_update(bt_ctx* c, const uint32_t* words, const float* params, cons
 }
 
 int bt_roi(bt_ctx* c, float* out, uint32_t nnodes) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     prof_begin(c);
     launch_roi_all(c->stream, dev_tree(c), c->roi.ptr);
@@ -942,6 +1004,7 @@ int bt_roi(bt_ctx* c, float* out, uint32_t nnodes) {
 }
 
 int bt_roi_upload(bt_ctx* c, const float* roi, uint32_t nnodes) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     if (!roi || nnodes != c->nnodes) return fail(BT_EINVAL, "roi must hold one value per node ordinal");
     BT_CUDA(cudaMemcpyAsync(c->roi.ptr, roi, nnodes * 4, cudaMemcpyHostToDevice, c->stream));
@@ -950,6 +1013,7 @@ int bt_roi_upload(bt_ctx* c, const float* roi, uint32_t nnodes) {
 }
 
 int bt_voi_build(bt_ctx* c, float margin) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     if (!c->haveRoi) return fail(BT_ESTATE, "no range of interest computed or uploaded");
     prof_begin(c);
@@ -960,6 +1024,7 @@ int bt_voi_build(bt_ctx* c, float margin) {
 }
 
 int bt_voi_upload(bt_ctx* c, const bt_voi* v, uint32_t n) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (n && !v) return fail(BT_EINVAL, "null volume buffer");
     std::vector<Voi> h(n);
@@ -985,6 +1050,7 @@ int bt_voi_upload(bt_ctx* c, const bt_voi* v, uint32_t n) {
 }
 
 int bt_voi_download(bt_ctx* c, bt_voi* out, uint32_t n) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (n > c->nvoi) return fail(BT_EINVAL, "more volumes requested than built");
     std::vector<Voi> h(n);
@@ -1013,6 +1079,7 @@ int bt_voi_download(bt_ctx* c, bt_voi* out, uint32_t n) {
 }
 
 int bt_abuffer_build(bt_ctx* c, const bt_camera* cam, uint32_t tile0, uint32_t tile1) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1025,10 +1092,11 @@ int bt_abuffer_build(bt_ctx* c, const bt_camera* cam, uint32_t tile0, uint32_t t
     if (rc) return rc;
     rc = do_abuffer(c, *cam, tile0, tile1, true);
     prof_end(c, 1);
-    return rc;
+    return rc ? rc : launch_status();
 }
 
 int bt_abuffer_info(bt_ctx* c, uint64_t* fragments, int32_t* tilesX, int32_t* tilesY) {
+    DevGuard dg_(c);
     if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     uint32_t total = 0;
@@ -1041,6 +1109,7 @@ int bt_abuffer_info(bt_ctx* c, uint64_t* fragments, int32_t* tilesX, int32_t* ti
 }
 
 int bt_abuffer_download(bt_ctx* c, uint32_t* offsets, bt_fragment* frags, uint64_t capacity) {
+    DevGuard dg_(c);
     if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     std::vector<uint32_t> off(tiles + 1);
@@ -1059,6 +1128,7 @@ int bt_abuffer_download(bt_ctx* c, uint32_t* offsets, bt_fragment* frags, uint64
 }
 
 int bt_abuffer_upload(bt_ctx* c, const bt_camera* cam, const uint32_t* offsets, const bt_fragment* frags) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1083,6 +1153,7 @@ int bt_abuffer_upload(bt_ctx* c, const bt_camera* cam, const uint32_t* offsets, 
 
 int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
              int exact) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1101,10 +1172,11 @@ int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint3
     prof_begin(c);
     rc = do_trace(c, *cam, *cfg, tile0, tile1, exact, true);
     prof_end(c, 2);
-    return rc;
+    return rc ? rc : launch_status();
 }
 
 int bt_normals(bt_ctx* c, const bt_camera* cam, int mode, int exact) {
+    DevGuard dg_(c);
     if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1116,10 +1188,11 @@ int bt_normals(bt_ctx* c, const bt_camera* cam, int mode, int exact) {
     }
     rc = do_normals(c, *cam, mode, exact);
     prof_end(c, 3);
-    return rc;
+    return rc ? rc : launch_status();
 }
 
 int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, int exact) {
+    DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1135,11 +1208,12 @@ int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cf
     BT_CUDA(cudaMemsetAsync(c->tileError.ptr, 0, c->tileError.cap, c->stream));
     c->haveGbuffer = true;
     c->viewsFrame = false;
-    return BT_OK;
+    return launch_status();
 }
 
 int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
                     int exact, int flags) {
+    DevGuard dg_(c);
     const bool use_graph = (flags & BT_FRAME_GRAPH) != 0;
     const bool normals = (flags & BT_FRAME_NO_NORMALS) == 0;
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
@@ -1192,7 +1266,10 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         if (r) return r;
         return normals ? do_normals(c, *cam, mode, exact) : BT_OK;
     };
-    if (!use_graph) return enqueue(true);
+    if (!use_graph) {
+        rc = enqueue(true);
+        return rc ? rc : launch_status();
+    }
 
     FrameKey key;
     std::memset(&key, 0, sizeof(key));
@@ -1205,6 +1282,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
     if (!c->haveGraph || !(key == c->graphKey)) {
         // eager, capacity-checked frame first (grows buffers), then capture
         rc = enqueue(true);
+        if (!rc) rc = launch_status();
         if (rc) return rc;
         BT_CUDA(cudaStreamSynchronize(c->stream));
         key.bufEpoch = c->bufEpoch;
@@ -1244,6 +1322,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
 }
 
 int bt_graph_kernel_count(bt_ctx* c, uint32_t* kernels, uint32_t* nodes) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (kernels) *kernels = c->haveGraph ? c->graphKernels : 0;
     if (nodes) *nodes = c->haveGraph ? c->graphNodes : 0;
@@ -1252,6 +1331,7 @@ int bt_graph_kernel_count(bt_ctx* c, uint32_t* kernels, uint32_t* nodes) {
 
 int bt_gbuffer_download(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
                         uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
+    DevGuard dg_(c);
     if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
     const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
     cudaStream_t s = c->stream;
@@ -1371,12 +1451,14 @@ int download_async(bt_ctx* c, void* const* planes, bool slab) {
 
 int bt_gbuffer_download_async(bt_ctx* c, uint8_t* hit, float* depth, float* normal, uint32_t* evalCount,
                               uint32_t* tileMaxOverlap, uint32_t* tileCacheBytes, uint8_t* tileError) {
+    DevGuard dg_(c);
     if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
     void* const planes[7] = {hit, depth, normal, evalCount, tileMaxOverlap, tileCacheBytes, tileError};
     return download_async(c, planes, false);
 }
 
 int bt_gbuffer_download_async_slab(bt_ctx* c, void* slab) {
+    DevGuard dg_(c);
     if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
     if (!slab) return fail(BT_EINVAL, "slab is null");
     size_t off[7], total = 0;
@@ -1388,6 +1470,7 @@ int bt_gbuffer_download_async_slab(bt_ctx* c, void* slab) {
 }
 
 int bt_gbuffer_layout(bt_ctx* c, size_t offsets[7], size_t* total) {
+    DevGuard dg_(c);
     if (!c || !offsets || !total) return fail(BT_EINVAL, "null argument");
     if (c->width <= 0 || c->height <= 0) return fail(BT_ESTATE, "no image size yet (upload a camera or render first)");
     const size_t px = (size_t)c->width * c->height, tiles = (size_t)c->tilesX * c->tilesY;
@@ -1402,6 +1485,7 @@ int bt_gbuffer_layout(bt_ctx* c, size_t offsets[7], size_t* total) {
 }
 
 int bt_set_tile_order(bt_ctx* c, const uint32_t* order, uint32_t n) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     if (n != tiles || !order) return fail(BT_EINVAL, "tile order must list every tile of the image once");
@@ -1419,6 +1503,7 @@ int bt_set_tile_order(bt_ctx* c, const uint32_t* order, uint32_t n) {
 }
 
 int bt_set_scheduling(bt_ctx* c, int mode) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (mode != 0 && mode != 1) return fail(BT_EINVAL, "scheduling mode must be 0 (raster) or 1 (longest-first)");
     c->schedMode = mode;
@@ -1427,6 +1512,7 @@ int bt_set_scheduling(bt_ctx* c, int mode) {
 }
 
 int bt_gbuffer_export(bt_ctx* c, bt_ipc_handles* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(BT_EINVAL, "null argument");
     if (!c->hit.ptr) return fail(BT_ESTATE, "no G-buffer allocated (render a frame first)");
     void* planes[6] = {c->hit.ptr, c->depth.ptr, c->evalCount.ptr, c->tileMaxOverlap.ptr, c->tileCacheBytes.ptr,
@@ -1443,6 +1529,7 @@ int bt_gbuffer_export(bt_ctx* c, bt_ipc_handles* out) {
 }
 
 int bt_gbuffer_import(bt_ctx* c, const bt_ipc_handles* in) {
+    DevGuard dg_(c);
     if (!c || !in) return fail(BT_EINVAL, "null argument");
     release_remote(c);
     for (int i = 0; i < 6; ++i) {
@@ -1464,12 +1551,14 @@ int bt_gbuffer_import(bt_ctx* c, const bt_ipc_handles* in) {
 }
 
 int bt_gbuffer_import_release(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     release_remote(c);
     return BT_OK;
 }
 
 int bt_download_wait(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     if (c->copyStream) BT_CUDA(cudaStreamSynchronize(c->copyStream));
     if (c->copyStream2) BT_CUDA(cudaStreamSynchronize(c->copyStream2));
@@ -1478,6 +1567,7 @@ int bt_download_wait(bt_ctx* c) {
 }
 
 int bt_gbuffer_device(bt_ctx* c, bt_gbuffer_view* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(BT_EINVAL, "null argument");
     out->hit = c->hit.ptr;
     out->depth = c->depth.ptr;
@@ -1494,6 +1584,7 @@ int bt_gbuffer_device(bt_ctx* c, bt_gbuffer_view* out) {
 }
 
 int bt_gbuffer_upload(bt_ctx* c, const bt_camera* cam, const uint8_t* hit, const float* depth) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     int rc = check_camera(cam);
     if (rc) return rc;
@@ -1509,6 +1600,7 @@ int bt_gbuffer_upload(bt_ctx* c, const bt_camera* cam, const uint8_t* hit, const
 }
 
 int bt_stats_download(bt_ctx* c, bt_stats* out) {
+    DevGuard dg_(c);
     if (!c || !out) return fail(BT_EINVAL, "null argument");
     uint64_t st[kStSlots];
     uint32_t cnt[kCntSlots];
@@ -1546,12 +1638,14 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
 }
 
 int bt_stats_reset(bt_ctx* c) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     BT_CUDA(cudaMemsetAsync(c->stats.ptr, 0, kStSlots * sizeof(uint64_t), c->stream));
     return BT_OK;
 }
 
 int bt_profile_enable(bt_ctx* c, int on) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     c->profiling = on != 0;
     for (int i = 0; i < kProfSlots; ++i) {
@@ -1564,6 +1658,7 @@ int bt_profile_enable(bt_ctx* c, int on) {
 int bt_profile_read(bt_ctx* c, float* ms4, uint32_t* l4) { return bt_profile_read_ex(c, ms4, l4, 4); }
 
 int bt_profile_read_ex(bt_ctx* c, float* ms, uint32_t* launches, uint32_t nslots) {
+    DevGuard dg_(c);
     if (!c) return fail(BT_EINVAL, "ctx is null");
     for (uint32_t i = 0; i < nslots && i < (uint32_t)kProfSlots; ++i) {
         if (ms) ms[i] = c->profMs[i];

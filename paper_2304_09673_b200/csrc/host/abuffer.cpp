@@ -57,7 +57,7 @@ TileABuffer rasterize_volumes(std::span<const VolumeOfInterest> volumes, const C
     out.tilesY = frame.tiles_y();
     const size_t tiles = static_cast<size_t>(out.tilesX) * out.tilesY;
     out.tiles.resize(tiles);
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     static_assert(sizeof(VolumeOfInterest) == sizeof(bt_voi), "VolumeOfInterest layout");
     std::vector<bt_voi> raw(volumes.size());
     for (size_t i = 0; i < volumes.size(); ++i) {

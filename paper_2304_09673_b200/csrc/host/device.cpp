@@ -45,6 +45,15 @@ bt_ctx* default_context() {
     return holder.ctx;
 }
 
+namespace {
+std::mutex& default_context_mutex() {
+    static std::mutex m;
+    return m;
+}
+}  // namespace
+
+ContextLease::ContextLease() : lock_(default_context_mutex()), ctx_(default_context()) {}
+
 bt_camera to_device_camera(const CameraFrame& frame) {
     bt_camera c;
     std::memset(&c, 0, sizeof(c));

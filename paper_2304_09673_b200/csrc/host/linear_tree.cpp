@@ -207,7 +207,7 @@ void upload_tree(bt_ctx* ctx, const LinearTree& tree) {
 std::vector<float> propagate_roi(const LinearTree& tree) {
     std::vector<float> roi(tree.nodes.size(), 0.0f);
     if (tree.nodes.empty()) return roi;
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     upload_tree(ctx, tree);
     check_device(bt_roi(ctx, roi.data(), tree.node_count()), "bt_roi");
     return roi;
@@ -225,7 +225,7 @@ std::vector<VolumeOfInterest> build_volumes_of_interest(const LinearTree& tree, 
         if (o >= roiUpper.size()) throw std::out_of_range("roiUpper has no entry for a primitive ordinal");
         roi[o] = roiUpper[o];
     }
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     upload_tree(ctx, tree);
     check_device(bt_roi_upload(ctx, roi.data(), tree.node_count()), "bt_roi_upload");
     check_device(bt_voi_build(ctx, margin), "bt_voi_build");

@@ -132,7 +132,7 @@ GBuffer render_tiles(const LinearTree& tree, const TileABuffer& abuffer, const C
     const Camera& cam = frame.camera();
     if (abuffer.tilesX != frame.tiles_x() || abuffer.tilesY != frame.tiles_y())
         throw std::invalid_argument("A-buffer tiling differs from the camera's");
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     upload_tree(ctx, tree);
     const size_t tiles = abuffer.tiles.size();
     std::vector<uint32_t> offsets(tiles + 1, 0);
@@ -154,7 +154,7 @@ GBuffer render_tiles(const LinearTree& tree, const TileABuffer& abuffer, const C
 GBuffer oracle_render(const LinearTree& tree, const CameraFrame& frame, const RenderConfig& cfg, RenderStats* stats) {
     validate_config(cfg);
     const Camera& cam = frame.camera();
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     upload_tree(ctx, tree);
     const bt_camera dcam = to_device_camera(frame);
     const bt_render_config dcfg = to_device_config(cfg);
@@ -173,7 +173,7 @@ void compute_normals(const LinearTree& tree, GBuffer& g, const CameraFrame& fram
     const Camera& cam = frame.camera();
     if (g.width != cam.width || g.height != cam.height)
         throw std::invalid_argument("G-buffer size differs from the camera's");
-    bt_ctx* ctx = default_context();
+    ContextLease ctx;
     upload_tree(ctx, tree);
     const bt_camera dcam = to_device_camera(frame);
     check_device(bt_gbuffer_upload(ctx, &dcam, g.hit.data(), g.depth.data()), "bt_gbuffer_upload");

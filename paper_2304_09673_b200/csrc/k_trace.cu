@@ -735,8 +735,18 @@ void* trace_fn(bool exact) {
     }
 }
 
+// Function attributes and occupancy are per device: cached per device index
+// (the C-ABI makes the context's device current before any launch).
+constexpr int kMaxDevices = 64;
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 || d >= kMaxDevices ? 0 : d;
+}
+
 uint32_t trace_grid_blocks(int smCount) {
-    static int perSM = 0;
+    static int perSMDev[kMaxDevices] = {};
+    int& perSM = perSMDev[current_device()];
     if (perSM == 0) {
         const size_t smem = sizeof(MarchSmem) * kTraceWarps;
         int best = 1;
@@ -780,7 +790,8 @@ void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& ca
     const size_t bytes = (size_t)t.nFrontier * 6 * sizeof(float) + (size_t)t.nUpper * sizeof(uint32_t);
     const uint32_t useSmem = bytes <= kGradSmemBytes ? 1u : 0u;
     const size_t smem = useSmem ? bytes : 0;
-    static bool attr = false;
+    static bool attrDev[kMaxDevices] = {};
+    bool& attr = attrDev[current_device()];
     if (!attr) {
         cudaFuncSetAttribute(k_gradient<ExactOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemBytes);
         cudaFuncSetAttribute(k_gradient<FastOps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGradSmemBytes);

@@ -240,6 +240,46 @@ NodePtr build_cells(uint32_t cells, uint32_t seed, float& diagOut) {
     return root;
 }
 
+// quad:N -- N lattice cells of 4 primitives, two of them random positive
+// definite quadrics, joined by compact unions (k = d = 0.21); every 5th cell
+// is carved by a compact difference with a quadric.  Cells merge by a left
+// comb of sharp unions.  Puts quadrics (the costliest primitive) on every
+// path of the tolerance-path parity tests at frame scale.
+NodePtr build_quads(uint32_t cells, uint32_t seed, float& diagOut) {
+    Rng r(seed ? seed : 11u);
+    uint32_t nx = 1, ny = 1, nz = 1;
+    while (nx * ny * nz < cells) {
+        if (nx <= ny && nx <= nz) ++nx;
+        else if (ny <= nz) ++ny;
+        else ++nz;
+    }
+    const float cell = 2.0f, scale = 0.42f;
+    const Vec3 origin{-0.5f * cell * (nx - 1), -0.5f * cell * (ny - 1), -0.5f * cell * (nz - 1)};
+    NodePtr root;
+    uint32_t placed = 0;
+    for (uint32_t z = 0; z < nz && placed < cells; ++z)
+        for (uint32_t y = 0; y < ny && placed < cells; ++y)
+            for (uint32_t x = 0; x < nx && placed < cells; ++x, ++placed) {
+                const Vec3 center = origin + Vec3{cell * x, cell * y, cell * z};
+                NodePtr sub;
+                for (int i = 0; i < 4; ++i) {
+                    PrimitiveParams pp = (i % 2 == 0)
+                                             ? random_quadric(r, Transform{center + r.vec(-0.3f, 0.3f), r.rot()})
+                                             : cell_primitive(r, center, scale);
+                    NodePtr next = prim(pp);
+                    sub = sub ? op(cunion(0.5f * scale, 0.5f * scale), std::move(sub), std::move(next))
+                              : std::move(next);
+                }
+                if (placed % 5 == 4)
+                    sub = op(cdiff(0.1f, 0.1f), std::move(sub),
+                             prim(random_quadric(r, Transform{center + Vec3{0.0f, 0.0f, -0.6f}, r.rot()})));
+                root = root ? op(sunion(), std::move(root), std::move(sub)) : std::move(sub);
+            }
+    const float sx = cell * nx, sy = cell * ny, sz = cell * nz;
+    diagOut = std::sqrt(sx * sx + sy * sy + sz * sz);
+    return root;
+}
+
 // C5: 4,000 primitives, left-heavy spine of 64 groups (depth ~70), each a
 // balanced compact-union tree (k = d = 0.08) with 25% compact-intersect
 // pairs (k = d = 0.05); every 9th spine operator is a compact difference.
@@ -365,6 +405,14 @@ std::unique_ptr<Scene> build(const std::string& name, uint32_t seed, int width, 
             units.push_back(prim(PrimitiveParams::sphere(1.0f + 0.002f * i, Transform{{0.001f * i, 0, 0}, Quat{}})));
         root = balanced(units, 0, units.size());
         sc->camera = look_at(Vec3{0, 0, -6}, origin, 0.1f, 40.0f, 64, 64);
+    } else if (name.rfind("quad:", 0) == 0) {
+        const uint32_t n = static_cast<uint32_t>(std::stoul(name.substr(5)));
+        if (n == 0) throw std::invalid_argument("quad:<cells> needs cells >= 1");
+        float diag = 0.0f;
+        root = build_quads(n, seed, diag);
+        const Vec3 dir = normalize(Vec3{0.9f, 0.55f, -1.25f});
+        const float dist = 0.6f * (1.35f * diag + 1.0f);
+        sc->camera = look_at(dir * dist, origin, 0.1f, 3.0f * diag + 4.0f, 1920, 1080);
     } else if (name.rfind("random:", 0) == 0) {
         const uint32_t n = static_cast<uint32_t>(std::stoul(name.substr(7)));
         Rng r(seed ? seed : 7u);
