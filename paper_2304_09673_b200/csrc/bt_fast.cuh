@@ -165,12 +165,12 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_quadric(e, g, h, l[i]);
     }
-    // the reference's NaN -> 0 filter (field.cpp:283).  Validated parameters
-    // and finite points never produce NaN in these closed forms, but trees
-    // uploaded straight through the C-ABI are not validated: keep the filter
-    // (one FSETP + FSEL per primitive value).
+    // the reference's NaN -> 0 filter (field.cpp:283), where a finite point
+    // can produce NaN (see fast_prim)
+    if (kind == 1u || kind == 4u) {
 #pragma unroll
-    for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(v[i]);
+        for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(v[i]);
+    }
 }
 
 // Operators on the fast path.  FMNMX-based min/max (fminf/fmaxf) instead of
@@ -219,6 +219,81 @@ BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
     if (code == 4u) return fmaxf(f0, f1);
     if (code == 5u) return fmaxf(f0, -f1);
     return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
+}
+
+// ---------------------------------------------------------------- view classes
+//
+// The interpreter below (eval_view_fast) pays per node for the header load,
+// the block address, prim/op tests, the kind and operator dispatch chains and
+// the two-register stack -- ~27 instructions per node, more than the field
+// arithmetic of the node on the small views that dominate (SURVEY.md appendix
+// C scenes: 98 % of C3's field evaluations are on views of <= 4 primitives).
+// The march therefore classifies each interval's view ONCE, when it is
+// staged, and runs a march loop specialised for its class:
+//   single  one primitive (20 % of C3's evaluations, 48 % of C1's): its kind
+//           and block live in registers for the whole interval;
+//   comb    a left comb P (P O)* -- every operator's right operand is the
+//           primitive just before it (78 % at C3): one 8-byte record per
+//           primitive (kind + block, operator code + block), no stack;
+//   general anything else: the interpreter.
+// Same formulas, same order of operations: the class only removes decoding.
+
+// A value every lane holds, made visibly warp-uniform: REDUX writes a
+// uniform register, so branches on it need no reconvergence barrier.  Used
+// once per interval (the single class's record), NOT per node: measured on
+// the per-node header reads (alternating A/B, scripts/ab_multi.sh) the
+// REDUX latency on the header -> block address -> parameter chain costs
+// more than the BSSY/BSYNC pairs it removes (C3 march +2.5 %, C2 / C5 +20 %).
+// All 32 lanes must call.
+BT_DEV uint32_t warp_uniform(uint32_t v) { return __reduce_or_sync(0xFFFFFFFFu, v); }
+
+// comb record of primitive j: x = (block float4 index << 3) | kind,
+// y = (operator block float4 index << 4) | operator code (j >= 1)
+BT_DEV uint32_t comb_prim_rec(uint32_t hdr) { return (((hdr & 0xFFFFu) >> 4) << 3) | blob_op(hdr); }
+BT_DEV uint32_t comb_op_rec(uint32_t hdr) { return (((hdr & 0xFFFFu) >> 4) << 4) | blob_op(hdr); }
+
+// One primitive value at one point; `kind` is warp-uniform.  The rigid
+// transform is shared by every rotated kind.
+//
+// The reference's NaN -> 0 filter (field.cpp:283) is applied where a NaN can
+// arise from a finite point: the ellipsoid (1/r of a zero radius times a zero
+// coordinate) and the sphere-cone (sqrt(1 - b^2) for |r0 - r1| >= h) when
+// their parameters bypassed validate_primitive (a tree uploaded straight
+// through the C-ABI).  Sphere, box, torus and quadric are closed forms of
+// finite values with no 0 * inf, inf - inf or sqrt of a negative: for finite
+// points and parameters (|.| < 1e18, no overflow) they never produce NaN, and
+// the filter there would cost 1.3 % of the march (measured, alternating A/B).
+// tests/test_gpu_reference_scale.py checks NaN-free FMA frames on every kind.
+BT_DEV float fast_prim(uint32_t kind, const float4* B, F3 p) {
+    if (kind == 0u) return f_sphere(B[0], p);
+    const F3 l = f_affine(B[0], B[1], B[2], p);
+    const float4 e = B[3];
+    if (kind == 3u) return f_box(e, l);
+    if (kind == 1u) return nan_to_zero(f_ellipsoid(e, B[4], l));
+    if (kind == 2u) return f_torus(e, l);
+    if (kind == 4u) return nan_to_zero(f_cone(e, B[4], l));
+    return f_quadric(e, B[4], B[5], l);
+}
+
+// operator of a comb step: compact and sharp unions first (the blobtree
+// generators' joins), the general chain otherwise
+BT_DEV float comb_op(uint32_t code, const float4* B, float f0, float f1) {
+    if (code == 9u) return fast_compact(0u, B, f0, f1);
+    if (code == 3u) return fminf(f0, f1);
+    return fast_operator(code, B, f0, f1);
+}
+
+BT_DEV float eval_comb(const uint2* rec, uint32_t nPrims, const float4* blk, F3 p) {
+    uint32_t rx = rec[0].x;
+    float v = fast_prim(rx & 7u, blk + (rx >> 3), p);
+    for (uint32_t j = 1; j < nPrims; ++j) {
+        const uint2 r = rec[j];
+        rx = r.x;
+        const uint32_t ry = r.y;
+        const float w = fast_prim(rx & 7u, blk + (rx >> 3), p);
+        v = comb_op(ry & 15u, blk + (ry >> 4), v, w);
+    }
+    return v;
 }
 
 constexpr uint32_t kNotAnOp = 0x80000000u;  // a primitive header: ends a fused primitive + operator pair

@@ -96,16 +96,20 @@ BT_DEV float eval_staged(const uint32_t* hdr, const uint32_t* word, uint32_t n, 
 }
 
 // --------------------------------------------------------------------------
-// Sphere-trace state machine (tracer.hpp:99-177).  phase: 0 finished,
-// 1 needs f(t0), 2 needs f(tn) (main step), 3 needs f(tb) (unrelaxed
-// back-off after an overshoot).  March arithmetic is always exact.
-
-// Compact march state: 6 floats + 2 words per ray (register pressure is
-// what limits the trace kernel's occupancy).  `st` packs the phase and the
-// flags; on completion `t` holds the hit position.  r = f / L is recomputed
-// where the reference reuses it (f is unchanged in between, same bits).
-constexpr uint32_t kPhaseMask = 3u;  // 0 done, 1 needs f(t0), 2 needs f(tn), 3 needs f(tb)
-constexpr uint32_t kRelax = 4u, kSaved = 8u, kHitFlag = 16u, kSlot1 = 32u;
+// Sphere-trace state machine (tracer.hpp:99-177), restated so that a ray
+// needs exactly one field value per lockstep step.  March arithmetic is
+// always exact (IEEE op by op), in both modes.
+//
+// State: the accepted sample (t, f), the end t1, the saved sphere
+// (savedT, savedF), the point being evaluated (evalT), and st:
+//   phase 0 done, 1 ACCEPT (f(t0), or a back-off sample: taken as is),
+//         2 MAIN (a step: overshoot-tested while relaxed);
+//   kSaved  a saved sphere is pending -- relaxation is off exactly while one
+//           is (relaxOn == !savedValid is an invariant of the reference loop,
+//           so one flag carries both);
+//   kHitFlag on completion: t holds the hit position.
+constexpr uint32_t kPhaseMask = 3u;
+constexpr uint32_t kSaved = 4u, kHitFlag = 8u;
 
 struct March {
     float t, f, t1, savedT, savedF, evalT;
@@ -115,108 +119,76 @@ struct March {
 BT_DEV uint32_t march_phase(const March& m) { return m.st & kPhaseMask; }
 BT_DEV bool march_hit(const March& m) { return (m.st & kHitFlag) != 0u; }
 
-BT_DEV void march_finish(March& m, bool hit, float t) {
-    m.st = (m.st & kSlot1) | (hit ? kHitFlag : 0u);
-    m.t = t;
-}
-
-BT_DEV void march_set_phase(March& m, uint32_t ph) { m.st = (m.st & ~kPhaseMask) | ph; }
-
-BT_DEV void march_idle(March& m, uint32_t slot) {
-    m.st = slot ? kSlot1 : 0u;
+BT_DEV void march_idle(March& m) {
+    m.st = 0u;
     m.evals = 0;
     m.t = 0.0f;
 }
 
-BT_DEV void march_begin(March& m, float t0, float t1, uint32_t slot) {
+BT_DEV void march_begin(March& m, float t0, float t1) {
     m.evals = 0;
-    m.st = (slot ? kSlot1 : 0u) | kRelax;
     m.t1 = t1;
-    if (t0 > t1) {
-        march_finish(m, false, 0.0f);
-        return;
-    }
-    m.t = t0;
+    m.t = 0.0f;
     m.evalT = t0;
-    march_set_phase(m, 1u);
+    m.st = t0 > t1 ? 0u : 1u;  // t0 > t1: an empty interval, a miss without evaluation
 }
 
-// One field value consumed (tracer.hpp:115-175), as straight-line selects.
-//
-// Every outcome of the reference loop body is one of:
-//   accept   the sample (evalT, v) becomes (t, f): phase 1 (f(t0)), phase 3
-//            (back-off sample), a trusted main step, or an overshoot whose
-//            back-off point tb already reaches the saved sphere (then
-//            t = savedT = tn, f = savedF = v and relaxation is back on -- the
-//            same state as a trusted step); then hit if v <= eps, miss if a
-//            main step reached t1, else advance: the next step from (t, f),
-//            clamped to t1.  While backing off, an advance that reaches the
-//            remembered sphere re-uses it (no evaluation): hit / miss tests on
-//            (savedT, savedF), then one more relaxed advance from there.
-//   back off an overshoot: save (tn, v), march unrelaxed from tb (phase 3),
-//            or miss when tb lies beyond t1
-// Everything is computed unconditionally and committed by predicates, so a
-// warp whose lanes end, hit, overshoot, back off or re-use a sphere in the
-// same iteration never diverges.  Arithmetic is the reference's, op for op.
+// One field value v = f(evalT) consumed.  The reference loop, per sample:
+//   MAIN, relaxed, overshoot ((tn-t)L >= f+|v| or v < -eps) -> save (tn, v),
+//        back off to tb = t + max(f/L, minStep): evaluate there (ACCEPT next),
+//        or, when tb already reaches the saved sphere, accept (tn, v) with
+//        relaxation on -- the same as a trusted step -- or miss beyond t1;
+//   otherwise the sample is accepted as (t, f): hit if v <= eps, else
+//   ADVANCE: miss if f/L is not finite; step = max(relaxed ? relax f/L : f/L,
+//        minStep); a step that reaches the saved sphere drops it (relaxation
+//        back on) and, when the sphere lies in [t + minStep, t1], RE-USES it
+//        without an evaluation: hit test on (savedT, savedF), then one more
+//        relaxed advance from there; finally the step is clamped to t1, and a
+//        sample already at t1 ends the march (a miss).
+// The reference's end test after a trusted main step (tn >= t1 -> miss) is
+// the clamp's "already at t1" case of the advance that follows, with the
+// same outcome and the same evaluation count.  Everything is computed
+// unconditionally and committed by predicates: a warp whose lanes hit,
+// miss, overshoot, back off or re-use a sphere in the same step never
+// diverges.
 BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
+    // Boolean algebra with & | (no short-circuit branches) and FMNMX for the
+    // step maxima: max(x, minStep) with minStep > 0 equals std::max except
+    // for a NaN x, and a NaN x only arises from a non-finite f/L, which ends
+    // the march before the step is used.
     m.evals++;
-    const uint32_t ph = m.st & kPhaseMask;
     const float tn = m.evalT;
-    const bool main = ph == 2u;
-    const bool relax = (m.st & kRelax) != 0u;
-    const bool saved = (m.st & kSaved) != 0u;
-    const bool ovBase = main && relax && (E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v)) || v < -tp.hitEps);
-    const float tb = E::add(m.t, smax(E::mul(m.f, tp.invL), tp.minStep));
-    const bool ov = ovBase && !(tb >= tn);
-    const bool acc = !ov;
-    const bool hitNow = acc && v <= tp.hitEps;
-    const bool endNow = acc && !hitNow && main && tn >= m.t1;
-    const bool stepOn = acc && !hitNow && !endNow;
-    // advance from the accepted sample (tn, v) with the current relaxation
+    const bool mainStep = (m.st & 2u) != 0u;
+    const bool sv = (m.st & kSaved) != 0u;
+    const float sT = m.savedT, sF = m.savedF;
+    const bool ovT = mainStep & !sv &
+                     ((E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v))) | (v < -tp.hitEps));
+    const float tb = E::add(m.t, fmaxf(E::mul(m.f, tp.invL), tp.minStep));
+    const bool ov = ovT & !(tb >= tn);
+    const bool hit1 = !ov & (v <= tp.hitEps);
+    // advance from the accepted (tn, v)
     const float r = E::mul(v, tp.invL);
     const bool fin = is_finite(r);
-    const float tnA = E::add(tn, smax(relax ? E::mul(tp.relax, r) : r, tp.minStep));
-    // ... reaching the remembered sphere while backing off
-    const bool reach = stepOn && fin && saved && tnA >= m.savedT;
-    const bool reuse = reach && m.savedT >= E::add(tn, tp.minStep) && m.savedT <= m.t1;
-    const bool hit2 = reuse && m.savedF <= tp.hitEps;
-    const bool end2 = reuse && !hit2 && m.savedT >= m.t1;
-    const float r2 = E::mul(m.savedF, tp.invL);
-    const float tn2 = E::add(m.savedT, smax(E::mul(tp.relax, r2), tp.minStep));  // relaxation is back on
-    const bool miss2 = reuse && !hit2 && !end2 && !is_finite(r2);
-    const bool step2 = reuse && !hit2 && !end2 && !miss2;
-    const bool beyond = tnA > m.t1;
-    const bool missAdv = stepOn && !reuse && (!fin || (beyond && tn >= m.t1));
-    const bool step1 = stepOn && !reuse && !missAdv;
-    const bool missOv = ov && tb > m.t1;
-    if (acc) {
-        m.t = tn;
-        m.f = v;
-    }
-    if (reuse) {
-        m.t = m.savedT;
-        m.f = m.savedF;
-    }
-    if (ov) {  // back off (phase 3) -- the saved sphere is only used when not missing
-        m.savedT = tn;
-        m.savedF = v;
-        m.evalT = tb;
-        m.st = (m.st & ~(kRelax | kPhaseMask)) | kSaved | 3u;
-    }
-    if (reach) m.st = (m.st & ~kSaved) | kRelax;
-    if (step1) {
-        m.evalT = beyond ? m.t1 : tnA;
-        m.st = (m.st & ~kPhaseMask) | 2u;
-    }
-    if (step2) {
-        m.evalT = tn2 > m.t1 ? m.t1 : tn2;
-        m.st = (m.st & ~kPhaseMask) | 2u;
-    }
-    if (hitNow || hit2) m.st = (m.st & kSlot1) | kHitFlag;  // t holds the hit (tn or savedT)
-    if (endNow || missAdv || missOv || end2 || miss2) {
-        m.st = m.st & kSlot1;
-        m.t = 0.0f;
-    }
+    const float tnA = E::add(tn, fmaxf(sv ? r : E::mul(tp.relax, r), tp.minStep));
+    const bool reach = sv & !hit1 & fin & (tnA >= sT);  // sv implies !ov
+    const bool reuse = reach & (sT >= E::add(tn, tp.minStep)) & (sT <= m.t1);
+    // ... re-using the saved sphere, then one relaxed advance from it
+    const float r2 = E::mul(sF, tp.invL);
+    const float tn2 = E::add(sT, fmaxf(E::mul(tp.relax, r2), tp.minStep));
+    const bool hit2 = reuse & (sF <= tp.hitEps);
+    const float T = reuse ? sT : tn;  // the accepted point the next step starts from
+    const float En = reuse ? tn2 : tnA;
+    const bool finN = is_finite(reuse ? r2 : r);
+    const bool beyond = En > m.t1;
+    const bool hit = hit1 | hit2;
+    const bool miss = (!ov & !hit & (!fin | !finN | (beyond & (T >= m.t1)))) | (ov & (tb > m.t1));
+    m.savedT = ov ? tn : sT;
+    m.savedF = ov ? v : sF;
+    m.t = ov ? m.t : T;
+    m.f = ov ? m.f : (reuse ? sF : v);
+    m.evalT = ov ? tb : (beyond ? m.t1 : En);
+    const uint32_t next = ((ov | (sv & !reach)) ? kSaved : 0u) | (ov ? 1u : 2u);
+    m.st = hit ? kHitFlag : (miss ? 0u : next);
 }
 
 }  // namespace btk

@@ -73,7 +73,10 @@ struct MarchSmem {
     float4 blocks[kMarchBlocks];  // fast parameter blocks of the staged view
     float4 rays[64];              // dir.xyz, dot(dir, forward) of the tile's rays
     uint32_t hdr[kViewCap];       // staged view: isPrim(1) op(5) | block byte offset
-    uint32_t word[kViewCap];      // exact path: tree word of each node's parameters
+    union {
+        uint32_t word[kViewCap + 1];      // exact path / raw parameters: tree word of each node
+        uint2 rec[(kViewCap + 1) / 2];    // fast path: comb records (bt_fast.cuh, comb_*_rec)
+    };
     float depth[64];
     uint32_t evals[64];
     uint8_t hit[64];
@@ -89,45 +92,58 @@ struct BlockStats {
     unsigned int maxOv, maxCache;
 };
 
-// March the pending rays of one interval over the staged view.
-template <class O>
+// View classes of the march loop (bt_fast.cuh, "view classes"): chosen once
+// per interval, so the per-step evaluation carries no class test.
+constexpr int kClsRaw = 0;      // raw tree parameters (exact path, or a view too large for the blocks)
+constexpr int kClsGeneral = 1;  // fast blocks, interpreter
+constexpr int kClsSingle = 2;   // fast blocks, one primitive
+constexpr int kClsComb = 3;     // fast blocks, left comb P (P O)*
+
+// March the pending rays of one interval over the staged view.  `aux`:
+// single -> the primitive's comb record; comb -> the primitive count.
+template <class O, int Cls>
 __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam, const TraceParams& tp, MarchSmem& s,
-                                               bool fits, uint32_t nView, uint32_t nPend, float vz0, float vz1,
+                                               uint32_t aux, uint32_t nView, uint32_t nPend, float vz0, float vz1,
                                                uint32_t lt, uint32_t& fe, uint32_t& fl, uint32_t& steps,
                                                uint32_t flops) {
+    const uint32_t uaux = warp_uniform(aux);  // class operand in a uniform register for the whole interval
     uint32_t cursor = 0, ray = kNoRay;
     March m;
-    march_idle(m, 0u);
+    march_idle(m);
     m.evalT = 0.0f;
     F3 dir{0.f, 0.f, 1.f};
     for (;;) {
+        // finished lanes are recorded and refilled only in steps where some
+        // lane is idle: while all 32 carry a ray, a step costs one ballot here
         const bool idle = march_phase(m) == 0u;
-        if (idle && ray != kNoRay) {  // record the ray that just finished
-            const uint32_t e = m.evals;
-            s.evals[ray] += e;
-            if (march_hit(m)) {
-                s.hit[ray] = 1;
-                s.depth[ray] = m.t;
-            }
-            fe += e;
-            fl += e * flops;
-            ray = kNoRay;
-        }
         const uint32_t idleMask = __ballot_sync(kFull, idle);
-        if (idleMask != 0u && cursor < nPend) {  // refill idle lanes from the queue
-            const uint32_t rank = cursor + __popc(idleMask & lt);
-            if (idle && rank < nPend) {
-                ray = s.pend[rank];
-                const float4 r = s.rays[ray];
-                dir = F3{r.x, r.y, r.z};
-                if (IsFast<O>::value) march_begin(m, vz0 * r.w, vz1 * r.w, 0u);  // r.w = 1 / dot(dir, forward)
-                else march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w), 0u);
+        if (idleMask != 0u) {
+            if (idle && ray != kNoRay) {  // record the ray that just finished
+                const uint32_t e = m.evals;
+                s.evals[ray] += e;
+                if (march_hit(m)) {
+                    s.hit[ray] = 1;
+                    s.depth[ray] = m.t;
+                }
+                fe += e;
+                fl += e * flops;
+                ray = kNoRay;
             }
-            cursor += __popc(idleMask);
-        }
-        if (!__any_sync(kFull, march_phase(m) != 0u)) {
-            if (cursor >= nPend) break;
-            continue;
+            if (cursor < nPend) {  // refill idle lanes from the queue
+                const uint32_t rank = cursor + __popc(idleMask & lt);
+                if (idle && rank < nPend) {
+                    ray = s.pend[rank];
+                    const float4 r = s.rays[ray];
+                    dir = F3{r.x, r.y, r.z};
+                    if (IsFast<O>::value) march_begin(m, vz0 * r.w, vz1 * r.w);  // r.w = 1 / dot(dir, forward)
+                    else march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w));
+                }
+                cursor += __popc(idleMask);
+            }
+            if (!__any_sync(kFull, march_phase(m) != 0u)) {
+                if (cursor >= nPend) break;
+                continue;
+            }
         }
         ++steps;
 #ifdef BT_STEP_HIST
@@ -138,7 +154,9 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
 #endif
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
-        if (IsFast<O>::value && fits) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
+        if constexpr (Cls == kClsSingle) v = fast_prim(uaux & 7u, s.blocks + (uaux >> 3), p);
+        else if constexpr (Cls == kClsComb) v = eval_comb(s.rec, uaux, s.blocks, p);
+        else if constexpr (Cls == kClsGeneral) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
         else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);  // exact path, or an oversized view
         if (march_phase(m) != 0u) march_consume(m, v, tp);
     }
@@ -210,13 +228,23 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             const uint32_t nView = ra.w & 0xFFFFu;
             // fast path: evaluation-ready parameter blocks in shared memory when
             // the view fits (the common case); otherwise raw parameters
-            const bool fits = rb.w <= kMarchBlocks;
+            const bool fits = IsFast<O>::value && rb.w <= kMarchBlocks;
+            bool notComb = false;
             for (uint32_t i = lane; i < nView; i += 32) {
                 const uint2 nd = vb.nodes[ra.z + i];
                 s.hdr[i] = nd.x;
-                s.word[i] = nd.y;
-                if (IsFast<O>::value && fits) convert_node(nd.x, t.words + nd.y + 1, s.blocks + ((nd.x & 0xFFFFu) >> 4));
+                if (fits) {
+                    convert_node(nd.x, t.words + nd.y + 1, s.blocks + ((nd.x & 0xFFFFu) >> 4));
+                    // left comb: node 0 and every odd node a primitive, every even node > 0 an operator
+                    const bool pr = blob_is_prim(nd.x);
+                    notComb |= i == 0u ? !pr : pr != ((i & 1u) != 0u);
+                    if (pr) s.rec[(i + 1u) >> 1].x = comb_prim_rec(nd.x);
+                    else s.rec[i >> 1].y = comb_op_rec(nd.x);
+                } else {
+                    s.word[i] = nd.y;
+                }
             }
+            const bool comb = fits && !__any_sync(kFull, notComb) && (nView & 1u);
             // queue of this interval: the tile's unfinished rays, in ray order
             const uint32_t p0 = ~found0, p1 = ~found1;
             const uint32_t c0 = __popc(p0), nPend = c0 + __popc(p1);
@@ -225,7 +253,21 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             __syncwarp();
             const float vz0 = view_z_from_ndc(cam, zb), vz1 = view_z_from_ndc(cam, ze);
             uint32_t ife = 0, ifl = 0, isteps = 0;
-            march_interval<O>(t, cam, tp, s, fits, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+            if constexpr (IsFast<O>::value) {
+                if (nView == 1u && comb)
+                    march_interval<O, kClsSingle>(t, cam, tp, s, s.rec[0].x, nView, nPend, vz0, vz1, lt, ife, ifl,
+                                                  isteps, rb.z);
+                else if (comb)
+                    march_interval<O, kClsComb>(t, cam, tp, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt, ife,
+                                                ifl, isteps, rb.z);
+                else if (fits)
+                    march_interval<O, kClsGeneral>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps,
+                                                   rb.z);
+                else
+                    march_interval<O, kClsRaw>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+            } else {
+                march_interval<O, kClsRaw>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+            }
             s.accFe[lane] += ife;
             s.accFl[lane] += ifl;
             s.accRnv[lane] += ife * nView;
@@ -643,16 +685,17 @@ __global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t
         __syncwarp();
         const F3 pc = vadd<E>(cam.pos, vscale<E>(F3{r.x, r.y, r.z}, depth));
         const float h = smax(1e-3f, E::mul(1e-4f, depth));
-        if (lane < 6) {
+        {  // lanes 0-5 evaluate the six taps; the whole warp runs the evaluator
+           // (its header reads are warp-uniform reductions: every lane must call)
             F3 tap = pc;
             const float s = (lane & 1) ? -h : h;
             if (lane < 2) tap.x = E::add(pc.x, s);
             else if (lane < 4) tap.y = E::add(pc.y, s);
-            else tap.z = E::add(pc.z, s);
+            else if (lane < 6) tap.z = E::add(pc.z, s);
             float v;
             if (fits) eval_view_fast<1>(sh[w], nView, blk[w], &tap, &v);
             else v = eval_staged<FastOps>(sh[w], sw[w], nView, t.words, tap);
-            res[w][lane] = v;
+            if (lane < 6) res[w][lane] = v;
         }
         __syncwarp();
         if (lane == 0) {
@@ -678,7 +721,7 @@ __global__ void k_oracle(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, GBuf 
         const float4 r = fb.rays[(size_t)tile * 64 + ((y & 7) << 3) + (x & 7)];
         const F3 d{r.x, r.y, r.z};
         March m;
-        march_begin(m, E::div(cam.nearZ, r.w), E::div(cam.farZ, r.w), 0u);
+        march_begin(m, E::div(cam.nearZ, r.w), E::div(cam.farZ, r.w));
         while (march_phase(m) != 0u) {
             const float v = eval_full<O>(t, ray_point<O>(cam.pos, d, m.evalT));
             march_consume(m, v, tp);
