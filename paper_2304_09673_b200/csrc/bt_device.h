@@ -11,6 +11,7 @@ namespace btk {
 
 // Superblock = 8x8 tiles (64x64 pixels): unit of the coarse cone cull.
 constexpr int kSB = 8;
+constexpr uint32_t kScanBlockElems = 4096;  // elements per block of the single-pass scan (k_frame.cu)
 
 struct DevTree {
     const float4* words = nullptr;
@@ -56,9 +57,17 @@ struct FrameBufs {
     uint32_t* tileLocal = nullptr;   // exclusive scan inside a 4096-tile block
     uint32_t* blockSum = nullptr;    // per scan block
     uint32_t* blockPrefix = nullptr; // exclusive over scan blocks (+ total at [nblocks])
-    uint32_t* offsets = nullptr;     // CSR [tiles+1]
+    uint32_t* offsets = nullptr;     // CSR [tiles+1] (built on demand for downloads, k_frag_csr)
     uint32_t* counters = nullptr;    // see kCnt*
-    uint64_t pairCap = 0, poolCap = 0;
+    // (volume, superblock) pairs grouped by superblock (k_tile's candidates)
+    uint32_t* sbCount = nullptr;     // [superblocks] pairs per superblock
+    uint32_t* sbCursor = nullptr;    // [superblocks] scatter cursors
+    uint32_t* sbLocal = nullptr;     // [superblocks] exclusive scan inside a scan block
+    uint32_t* sbBlockSum = nullptr;
+    uint32_t* sbBlockPrefix = nullptr;
+    uint32_t* sbList = nullptr;      // [pairCap] volume indices, superblock-major
+    uint2* tileFrag = nullptr;       // [tiles] (first fragment, count) of each tile's sorted list in frags
+    uint64_t pairCap = 0, poolCap = 0, fragCap = 0;
 };
 
 // device counters (uint32 slots)
@@ -70,7 +79,10 @@ enum : int {
     kCntFallback = 4,
     kCntOverflow = 5,
     kCntFallbackHard = 6,  // fast-path fallbacks without a usable view (full-tree gradient)
-    kCntSlots = 8
+    kCntFrags = 7,         // fragments allocated (k_tile bump allocator)
+    kCntScanDone2 = 8,     // completion counter of the superblock scan
+    kCntTileQueue = 9,     // k_tile work queue head
+    kCntSlots = 12
 };
 
 // device statistics (uint64 slots)
@@ -132,7 +144,18 @@ uint32_t camera_tile_cover(int tilesX, int tilesY, uint32_t tile0, uint32_t tile
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
                     const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
                     int smCount, bool zero = true);
-void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
+// k_tile, warp per tile of [tile0, tile1): raster (the tile's candidate
+// volumes from its superblock's pair list, exact ray tests, sorted fragment
+// list) and / or views (fetch sequence -> interval records + active words).
+constexpr uint32_t kTileRaster = 1u, kTileViews = 2u;
+void launch_tile_pass(cudaStream_t st, uint32_t mode, const Cam& cam, const TraceParams& tp, const Voi* vois,
+                      const FrameBufs& fb, const ViewBufs& vb, int tilesX, int tilesY, uint32_t tile0,
+                      uint32_t tile1, int smCount);
+// the A-buffer's CSR (fb.offsets, fragments in tile order in fb.unsorted as Frag) for a download
+void launch_frag_csr(cudaStream_t st, const FrameBufs& fb, uint32_t tiles, int smCount);
+// tileFrag from CSR offsets (an uploaded A-buffer)
+void launch_tile_frag_from_offsets(cudaStream_t st, const FrameBufs& fb, uint32_t tiles);
+uint32_t superblock_count(int tilesX, int tilesY);
 
 // ---- launchers (k_util.cu) -------------------------------------------
 void launch_copy_segments(cudaStream_t st, const void* const* src, void* const* dst, const size_t* bytes, int n,
@@ -144,14 +167,8 @@ void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWor
                          uint32_t n, int32_t* scratch);
 
 // ---- launchers (k_views.cu) -------------------------------------------
-// build=false: count pass + scan (the host may then read the totals and grow
-// the record buffers); build=true: write the interval/view records.
-// zero = false (every launcher): the frame's counters were already zeroed at
-// the start of a captured frame, off the critical path.
-void launch_views(cudaStream_t st, const DevTree& t, const Cam& cam, const TraceParams& tp, const FrameBufs& fb,
-                  const ViewBufs& vb, uint32_t tiles, uint32_t tile0, uint32_t tile1, bool build, bool zero = true);
-uint32_t view_scan_blocks(uint32_t tiles);
-size_t view_slab_words(uint32_t tiles);
+// k_view_build over the records k_tile allocated (thread per interval)
+void launch_view_build(cudaStream_t st, const DevTree& t, const ViewBufs& vb);
 // longest-first march units of [tile0, tile1) from vb.tileCost (hist: 258 words of
 // scratch, [257] = unit count); tiles costing >= beta x the average work per
 // warp (at most cap of them) become two half-tile units

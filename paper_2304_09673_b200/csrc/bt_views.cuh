@@ -53,20 +53,19 @@ struct ViewBufs {
     uint32_t* slab = nullptr;      // [tiles * slab stride] count-pass intervals (k_views.cu)
     const uint32_t* order = nullptr;  // optional march units in order (tile | kUnitSplit | kUnitPart1), else raster
     const uint32_t* unitCount = nullptr;  // number of entries of `order` (device)
-    uint32_t* tileCost = nullptr;     // [tiles] march cost proxy 0..255 (k_view_count; scheduling)
+    uint32_t* tileCost = nullptr;     // [tiles] march cost proxy 0..255 (k_tile; scheduling)
+    uint2* base = nullptr;            // [tiles] (first interval record, first view node) of the tile
     uint64_t ivCap = 0, nodeCap = 0;
 };
+// vb.counters: [1] overflow flag, [2] interval records allocated, [3] view nodes allocated
 
 constexpr uint32_t kViewScanBlock = 4096;
 constexpr uint32_t kUnitSplit = 0x80000000u;  // march unit = half a tile (one pixel-column parity)
 constexpr uint32_t kUnitPart1 = 0x40000000u;  // ... the odd columns
 constexpr uint32_t kUnitTile = 0x3FFFFFFFu;  // tiles per scan block of k_view_scan
 
-// exclusive (interval, node) offsets of a tile
-BT_DEV uint2 view_offset(const ViewBufs& vb, uint32_t tile) {
-    const uint2 l = vb.local[tile], p = vb.blockPrefix[tile / kViewScanBlock];
-    return make_uint2(l.x + p.x, l.y + p.y);
-}
+// (interval, node) offsets of a tile's records (bump-allocated by k_tile)
+BT_DEV uint2 view_offset(const ViewBufs& vb, uint32_t tile) { return vb.base[tile]; }
 
 // ---------------------------------------------------------------- warp fetch
 // fetch_interval (tracer.cpp:50-103; TileFetchState, tracer.hpp:62-84),

@@ -125,6 +125,9 @@ struct bt_ctx {
     DevBuf<uint4> pool, unsorted;
     DevBuf<Frag> frags;
     DevBuf<uint32_t> tileCount, tileCursor, tileLocal, blockSum, blockPrefix, offsets, counters;
+    // (volume, superblock) pairs grouped by superblock, per-tile fragment lists
+    DevBuf<uint32_t> sbCount, sbCursor, sbLocal, sbBlockSum, sbBlockPrefix, sbList;
+    DevBuf<uint2> tileFrag;
     bool haveAbuffer = false;
     bool haveRays = false;
     bt_camera rayCam{};
@@ -153,9 +156,9 @@ struct bt_ctx {
 
     DevBuf<uint64_t> stats;
     // compiled intervals / pruned views of stage (c) (k_views.cu)
-    DevBuf<uint2> vCount, vLocal, vBlockSum, vBlockPrefix, vNodes;
+    DevBuf<uint2> vCount, vBase, vNodes;
     DevBuf<IntervalRec> vIv;
-    DevBuf<uint32_t> vCounters, vSlab;
+    DevBuf<uint32_t> vCounters;
     // march scheduling: 0 raster, 1 longest-first by cost proxy (default), 2 host order
     DevBuf<uint32_t> tileOrder, tileCost, orderHist, hostUnits;
     bool viewsFrame = false;  // the G-buffer came from a whole-frame FMA-path march (its records are valid)
@@ -241,21 +244,26 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.blockPrefix = c->blockPrefix.ptr;
     f.offsets = c->offsets.ptr;
     f.counters = c->counters.ptr;
-    f.pairCap = c->pairs.cap;
-    f.poolCap = c->pool.cap;
+    f.sbCount = c->sbCount.ptr;
+    f.sbCursor = c->sbCursor.ptr;
+    f.sbLocal = c->sbLocal.ptr;
+    f.sbBlockSum = c->sbBlockSum.ptr;
+    f.sbBlockPrefix = c->sbBlockPrefix.ptr;
+    f.sbList = c->sbList.ptr;
+    f.tileFrag = c->tileFrag.ptr;
+    f.pairCap = std::min(c->pairs.cap, c->sbList.cap);
+    f.poolCap = c->frags.cap;
+    f.fragCap = std::min(c->frags.cap, c->unsorted.cap);
     return f;
 }
 
 ViewBufs view_bufs(const bt_ctx* c) {
     ViewBufs v;
     v.count = c->vCount.ptr;
-    v.local = c->vLocal.ptr;
-    v.blockSum = c->vBlockSum.ptr;
-    v.blockPrefix = c->vBlockPrefix.ptr;
+    v.base = c->vBase.ptr;
     v.iv = c->vIv.ptr;
     v.nodes = c->vNodes.ptr;
     v.counters = c->vCounters.ptr;
-    v.slab = c->vSlab.ptr;
     v.order = nullptr;  // chosen per trace (do_trace)
     v.tileCost = c->tileCost.ptr;
     v.ivCap = c->vIv.cap;
@@ -348,13 +356,16 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->tileMaxOverlap.reserve(tiles));
     BT_CUDA(c->tileCacheBytes.reserve(tiles));
     BT_CUDA(c->tileError.reserve(tiles));
-    const size_t nvscan = view_scan_blocks((uint32_t)tiles);
     BT_CUDA(c->vCount.reserve(tiles));
-    BT_CUDA(c->vLocal.reserve(tiles));
-    BT_CUDA(c->vBlockSum.reserve(nvscan));
-    BT_CUDA(c->vBlockPrefix.reserve(nvscan + 1));
-    BT_CUDA(c->vCounters.reserve(2));
-    BT_CUDA(c->vSlab.reserve(view_slab_words((uint32_t)tiles)));
+    BT_CUDA(c->vBase.reserve(tiles));
+    BT_CUDA(c->vCounters.reserve(4));
+    const size_t nsbscan = (nsb + kScanBlockElems - 1) / kScanBlockElems;
+    BT_CUDA(c->sbCount.reserve(nsb));
+    BT_CUDA(c->sbCursor.reserve(nsb));
+    BT_CUDA(c->sbLocal.reserve(nsb));
+    BT_CUDA(c->sbBlockSum.reserve(nsbscan));
+    BT_CUDA(c->sbBlockPrefix.reserve(nsbscan + 1));
+    BT_CUDA(c->tileFrag.reserve(tiles));
     BT_CUDA(c->tileCost.reserve(tiles));
     BT_CUDA(c->tileOrder.reserve(tiles * 2));
     BT_CUDA(c->orderHist.reserve(258));
@@ -371,10 +382,10 @@ int ensure_frame_caps(bt_ctx* c, size_t pairCap, size_t poolCap) {
     bool moved = false;
     if (pairCap > c->pairs.cap) {
         BT_CUDA(c->pairs.reserve(pairCap));
+        BT_CUDA(c->sbList.reserve(pairCap));
         moved = true;
     }
-    if (poolCap > c->pool.cap) {
-        BT_CUDA(c->pool.reserve(poolCap));
+    if (poolCap > c->frags.cap) {  // the fragment store (and its CSR / overflow staging)
         BT_CUDA(c->unsorted.reserve(poolCap));
         BT_CUDA(c->frags.reserve(poolCap));
         moved = true;
@@ -460,34 +471,79 @@ int resolve_tiles(bt_ctx* c, uint32_t& tile0, uint32_t& tile1) {
     return BT_OK;
 }
 
-// Launch the A-buffer kernels; in `checked` mode verify the capacities
-// afterwards (one D2H of the counters) and rebuild after growing.
-int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, bool checked) {
+int ensure_view_caps(bt_ctx* c) {
+    if (c->vIv.cap == 0) {
+        const size_t tiles = (size_t)c->tilesX * c->tilesY;
+        BT_CUDA(c->vIv.reserve(std::max<size_t>(1u << 16, tiles * 2)));
+        BT_CUDA(c->vNodes.reserve(std::max<size_t>(1u << 18, tiles * 8)));
+        c->bufEpoch++;
+    }
+    return BT_OK;
+}
+
+// The A-buffer: superblock pairs, then the per-tile pass (k_tile) in `mode`
+// (raster, or raster + the interval records of `tp` in a fused frame).  In
+// `checked` mode the allocation counters are read back afterwards (one D2H)
+// and the frame rebuilt after growing what overflowed; inside a graph replay
+// an overflow degrades to an empty, flagged A-buffer / record set.
+int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, bool checked,
+               uint32_t mode = kTileRaster, const TraceParams* tp = nullptr) {
     if (c->pairs.cap == 0) {
         int rc = ensure_frame_caps(c, std::max<size_t>(1u << 18, (size_t)c->nvoi * 16), 1u << 20);
         if (rc) return rc;
     }
+    if (mode & kTileViews) {
+        int rc = ensure_view_caps(c);
+        if (rc) return rc;
+    }
+    const TraceParams tpv = tp ? *tp : TraceParams{};
     for (int attempt = 0; attempt < 8; ++attempt) {
         launch_abuffer(c->stream, to_cam(cam), c->vois.ptr, c->nvoi, frame_bufs(c), c->tilesX, c->tilesY,
                        tile0, tile1, c->smCount, !c->prezeroed);
+        launch_tile_pass(c->stream, mode, to_cam(cam), tpv, c->vois.ptr, frame_bufs(c), view_bufs(c), c->tilesX,
+                         c->tilesY, tile0, tile1, c->smCount);
         if (!checked) break;
         uint32_t cnt[kCntSlots];
+        uint32_t vc[4] = {0u, 0u, 0u, 0u};
         BT_CUDA(cudaMemcpyAsync(cnt, c->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+        if (mode & kTileViews)
+            BT_CUDA(cudaMemcpyAsync(vc, c->vCounters.ptr, sizeof(vc), cudaMemcpyDeviceToHost, c->stream));
         BT_CUDA(cudaStreamSynchronize(c->stream));
-        const bool pairOver = cnt[kCntPairs] > c->pairs.cap;
-        const bool poolOver = cnt[kCntPool] > c->pool.cap;
-        // a dropped pair also drops its fragments: grow the pool with it
-        if (pairOver && !poolOver) {
-            int rc = ensure_frame_caps(c, (size_t)cnt[kCntPairs] * 2, c->pool.cap * 2);
-            if (rc) return rc;
-            continue;
-        }
-        if (!pairOver && !poolOver) break;
+        const bool pairOver = cnt[kCntPairs] > frame_bufs(c).pairCap;
+        const bool fragOver = !pairOver && cnt[kCntFrags] > frame_bufs(c).fragCap;
+        const bool ivOver = !pairOver && !fragOver && (mode & kTileViews) && (vc[2] > c->vIv.cap || vc[3] > c->vNodes.cap);
+        if (!pairOver && !fragOver && !ivOver) break;
+        // (lost pairs also lose their fragments and records: grow one thing at a time)
         int rc = ensure_frame_caps(c, pairOver ? (size_t)cnt[kCntPairs] * 2 : c->pairs.cap,
-                                   poolOver ? (size_t)cnt[kCntPool] * 2 : c->pool.cap);
+                                   fragOver ? (size_t)cnt[kCntFrags] * 2 : c->frags.cap);
         if (rc) return rc;
+        if (ivOver) {
+            if (vc[2] > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)vc[2] * 2));
+            if (vc[3] > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)vc[3] * 2));
+            c->bufEpoch++;
+        }
     }
     c->haveAbuffer = true;
+    return BT_OK;
+}
+
+// The interval records of an A-buffer built without them (bt_abuffer_build
+// or an uploaded A-buffer, then bt_trace): k_tile in views mode, checked.
+int do_views(bt_ctx* c, const bt_camera& cam, const TraceParams& tp, uint32_t tile0, uint32_t tile1, bool checked) {
+    int rc = ensure_view_caps(c);
+    if (rc) return rc;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        launch_tile_pass(c->stream, kTileViews, to_cam(cam), tp, c->vois.ptr, frame_bufs(c), view_bufs(c), c->tilesX,
+                         c->tilesY, tile0, tile1, c->smCount);
+        if (!checked) break;
+        uint32_t vc[4];
+        BT_CUDA(cudaMemcpyAsync(vc, c->vCounters.ptr, sizeof(vc), cudaMemcpyDeviceToHost, c->stream));
+        BT_CUDA(cudaStreamSynchronize(c->stream));
+        if (vc[2] <= c->vIv.cap && vc[3] <= c->vNodes.cap) break;
+        if (vc[2] > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)vc[2] * 2));
+        if (vc[3] > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)vc[3] * 2));
+        c->bufEpoch++;
+    }
     return BT_OK;
 }
 
@@ -504,22 +560,18 @@ float split_beta() {
     return beta;
 }
 
-// Stage (c): compile the tiles' intervals and views (count, scan, build), then
-// march.  In `checked` mode the record totals are read back after the scan
-// and the record buffers grown (2x headroom) before the build; inside a graph
-// replay an overflow is flagged (bt_stats_download) and the tiles marked.
+// Stage (c): the interval records (unless the fused A-buffer pass already
+// wrote them), the views (k_view_build) beside the march order, then the
+// march.  In `checked` mode the record totals are read back and the buffers
+// grown (2x headroom); inside a graph replay an overflow is flagged
+// (bt_stats_download) and the tiles marked.
 int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
-             int exact, bool checked) {
+             int exact, bool checked, bool haveRecords = false) {
     if (c->tileQueue.cap == 0) {
         BT_CUDA(c->tileQueue.reserve(1));
         c->bufEpoch++;
     }
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
-    if (c->vIv.cap == 0) {
-        BT_CUDA(c->vIv.reserve(std::max<size_t>(1u << 16, (size_t)tiles * 2)));
-        BT_CUDA(c->vNodes.reserve(std::max<size_t>(1u << 18, (size_t)tiles * 8)));
-        c->bufEpoch++;
-    }
     const DevTree t = dev_tree(c);
     const Cam k = to_cam(cam);
     const TraceParams tp = trace_params(cfg, cam);
@@ -527,31 +579,19 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     // stream capture would invalidate the capture
     const bool prof = c->profiling && checked;
     if (prof) cudaEventRecord(c->ev[2], c->stream);
-    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false, !c->prezeroed);
-    // longest-first march units from the count pass's cost proxy; in a captured
-    // frame they are ordered on the side stream while the views are built
+    if (!haveRecords) {
+        int rc = do_views(c, cam, tp, tile0, tile1, checked);
+        if (rc) return rc;
+    }
+    // longest-first march units from k_tile's cost proxy; in a captured frame
+    // they are ordered on the side stream while the views are built
     auto order = [&](cudaStream_t st) {
         launch_tile_order(st, view_bufs(c), trace_gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
                           trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
     };
     const bool forkOrder = c->schedMode == 1 && !checked;
-    if (c->schedMode == 1 && checked) order(c->stream);  // overlaps the host's readback below
-    if (prof) cudaEventRecord(c->ev[3], c->stream);  // (the readback is not stage time)
-    if (checked) {  // the totals: grow the record buffers and recount if short
-        uint2 total{0u, 0u};
-        BT_CUDA(cudaMemcpyAsync(&total, c->vBlockPrefix.ptr + view_scan_blocks(tiles), sizeof(uint2),
-                                cudaMemcpyDeviceToHost, c->stream));
-        BT_CUDA(cudaStreamSynchronize(c->stream));
-        if (total.x > c->vIv.cap || total.y > c->vNodes.cap) {
-            if (total.x > c->vIv.cap) BT_CUDA(c->vIv.reserve((size_t)total.x * 2));
-            if (total.y > c->vNodes.cap) BT_CUDA(c->vNodes.reserve((size_t)total.y * 2));
-            c->bufEpoch++;
-            launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, false);
-            // the recount rewrote tileCost, which the ordering zeroes on split
-            // tiles (their once-only error count): order again
-            if (c->schedMode == 1) order(c->stream);
-        }
-    }
+    if (c->schedMode == 1 && checked) order(c->stream);
+    if (prof) cudaEventRecord(c->ev[3], c->stream);
     if (forkOrder) {
         int rc = ensure_side(c);
         if (rc) return rc;
@@ -561,7 +601,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     }
     if (prof) cudaEventRecord(c->ev[4], c->stream);
-    launch_views(c->stream, t, k, tp, frame_bufs(c), view_bufs(c), tiles, tile0, tile1, true);
+    launch_view_build(c->stream, t, view_bufs(c));
     if (prof) cudaEventRecord(c->ev[5], c->stream);
     if (forkOrder) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[1], 0));
     ViewBufs vbm = view_bufs(c);
@@ -574,7 +614,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     }
     launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, trace_gbuf(c), c->stats.ptr, tile0, tile1,
                  c->smCount, c->tileQueue.ptr, !c->prezeroed);
-    if (prof) {  // sub-stage split: views (count+scan, build) and the march alone
+    if (prof) {  // sub-stage split: views (records, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
         cudaEventSynchronize(c->ev[1]);
         float a = 0.f, b = 0.f, m = 0.f;
@@ -688,10 +728,10 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->normal.release();
     c->stats.release();
     c->gradScratch.release();
-    for (auto* b : {&c->vCount, &c->vLocal, &c->vBlockSum, &c->vBlockPrefix, &c->vNodes}) b->release();
+    for (auto* b : {&c->vCount, &c->vBase, &c->vNodes, &c->tileFrag}) b->release();
+    for (auto* b : {&c->sbCount, &c->sbCursor, &c->sbLocal, &c->sbBlockSum, &c->sbBlockPrefix, &c->sbList}) b->release();
     c->vIv.release();
     c->vCounters.release();
-    c->vSlab.release();
     c->tileOrder.release();
     c->tileCost.release();
     c->hostUnits.release();
@@ -1095,14 +1135,24 @@ int bt_abuffer_build(bt_ctx* c, const bt_camera* cam, uint32_t tile0, uint32_t t
     return rc ? rc : launch_status();
 }
 
+// The A-buffer as CSR for a download: the per-tile lists (bump order in
+// fb.frags) are compacted into tile order on the device (k_frag_csr).
+int abuffer_csr(bt_ctx* c, std::vector<uint32_t>& off) {
+    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
+    launch_frag_csr(c->stream, frame_bufs(c), tiles, c->smCount);
+    off.resize(tiles + 1);
+    BT_CUDA(cudaMemcpyAsync(off.data(), c->offsets.ptr, (tiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    return launch_status();
+}
+
 int bt_abuffer_info(bt_ctx* c, uint64_t* fragments, int32_t* tilesX, int32_t* tilesY) {
     DevGuard dg_(c);
     if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
-    const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
-    uint32_t total = 0;
-    BT_CUDA(cudaMemcpyAsync(&total, c->offsets.ptr + tiles, 4, cudaMemcpyDeviceToHost, c->stream));
-    BT_CUDA(cudaStreamSynchronize(c->stream));
-    if (fragments) *fragments = total;
+    std::vector<uint32_t> off;
+    const int rc = abuffer_csr(c, off);
+    if (rc) return rc;
+    if (fragments) *fragments = off.back();
     if (tilesX) *tilesX = c->tilesX;
     if (tilesY) *tilesY = c->tilesY;
     return BT_OK;
@@ -1112,15 +1162,15 @@ int bt_abuffer_download(bt_ctx* c, uint32_t* offsets, bt_fragment* frags, uint64
     DevGuard dg_(c);
     if (!c || !c->haveAbuffer) return fail(BT_ESTATE, "no A-buffer built");
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
-    std::vector<uint32_t> off(tiles + 1);
-    BT_CUDA(cudaMemcpyAsync(off.data(), c->offsets.ptr, (tiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
-    BT_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<uint32_t> off;
+    const int rc = abuffer_csr(c, off);
+    if (rc) return rc;
     if (offsets) std::memcpy(offsets, off.data(), (tiles + 1) * 4);
     if (frags) {
         if (capacity < off[tiles]) return fail(BT_EINVAL, "fragment capacity too small");
         static_assert(sizeof(bt_fragment) == sizeof(Frag), "fragment layout");
         if (off[tiles])
-            BT_CUDA(cudaMemcpyAsync(frags, c->frags.ptr, (size_t)off[tiles] * sizeof(Frag), cudaMemcpyDeviceToHost,
+            BT_CUDA(cudaMemcpyAsync(frags, c->unsorted.ptr, (size_t)off[tiles] * sizeof(Frag), cudaMemcpyDeviceToHost,
                                     c->stream));
         BT_CUDA(cudaStreamSynchronize(c->stream));
     }
@@ -1145,10 +1195,11 @@ int bt_abuffer_upload(bt_ctx* c, const bt_camera* cam, const uint32_t* offsets, 
     BT_CUDA(cudaMemcpyAsync(c->offsets.ptr, offsets, (tiles + 1) * 4, cudaMemcpyHostToDevice, c->stream));
     if (total)
         BT_CUDA(cudaMemcpyAsync(c->frags.ptr, frags, (size_t)total * sizeof(Frag), cudaMemcpyHostToDevice, c->stream));
-    launch_offsets_from_counts(c->stream, frame_bufs(c), tiles);
+    launch_tile_frag_from_offsets(c->stream, frame_bufs(c), tiles);
+    BT_CUDA(cudaMemcpyAsync(c->counters.ptr + kCntFrags, &total, 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->haveAbuffer = true;
-    return BT_OK;
+    return launch_status();
 }
 
 int bt_trace(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, uint32_t tile0, uint32_t tile1,
@@ -1244,11 +1295,10 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
             if (r) return r;
             // the frame's counters and per-tile cursors, zeroed here instead of
             // in front of each stage
-            const size_t tiles = (size_t)c->tilesX * c->tilesY;
+            const size_t nsb = superblock_count(c->tilesX, c->tilesY);
             BT_CUDA(cudaMemsetAsync(c->counters.ptr, 0, kCntSlots * sizeof(uint32_t), c->side));
-            BT_CUDA(cudaMemsetAsync(c->tileCount.ptr, 0, tiles * sizeof(uint32_t), c->side));
-            BT_CUDA(cudaMemsetAsync(c->tileCursor.ptr, 0, tiles * sizeof(uint32_t), c->side));
-            BT_CUDA(cudaMemsetAsync(c->vCounters.ptr, 0, 2 * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->sbCount.ptr, 0, nsb * sizeof(uint32_t), c->side));
+            BT_CUDA(cudaMemsetAsync(c->sbCursor.ptr, 0, nsb * sizeof(uint32_t), c->side));
             BT_CUDA(cudaMemsetAsync(c->tileQueue.ptr, 0, sizeof(uint32_t), c->side));
             BT_CUDA(cudaEventRecord(c->evJoin[0], c->side));
             c->prezeroed = true;
@@ -1260,9 +1310,11 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         if (checked) r = do_camera(c, *cam, c0, c1);
         else BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[0], 0));
         if (r) return r;
-        r = do_abuffer(c, *cam, tile0, tile1, checked);
+        // one per-tile pass builds each tile's fragment list AND its interval records
+        const TraceParams tp = trace_params(*cfg, *cam);
+        r = do_abuffer(c, *cam, tile0, tile1, checked, kTileRaster | kTileViews, &tp);
         if (r) return r;
-        r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked);
+        r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked, true);
         if (r) return r;
         return normals ? do_normals(c, *cam, mode, exact) : BT_OK;
     };
@@ -1619,14 +1671,8 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
     out->tileErrors = st[kStTileErrors];
     out->normalFallbacks = st[kStFallbacks];
     out->warpSteps = st[kStWarpSteps];
-    if (c->haveAbuffer) {
-        const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
-        uint32_t total = 0;
-        BT_CUDA(cudaMemcpyAsync(&total, c->offsets.ptr + tiles, 4, cudaMemcpyDeviceToHost, c->stream));
-        BT_CUDA(cudaStreamSynchronize(c->stream));
-        out->fragments = total;
-    }
-    if (cnt[kCntOverflow] || cnt[kCntPairs] > c->pairs.cap)
+    if (c->haveAbuffer) out->fragments = cnt[kCntFrags];  // the per-tile lists' total (k_tile)
+    if (cnt[kCntOverflow] || cnt[kCntPairs] > frame_bufs(c).pairCap)
         return fail(BT_ENOMEM, "A-buffer capacity overflowed during a graph replay; re-run eagerly");
     if (c->vCounters.ptr) {
         uint32_t vc[2] = {0u, 0u};

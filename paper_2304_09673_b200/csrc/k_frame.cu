@@ -4,26 +4,28 @@
 //   k_roi_all        range of interest per node                 (linear_tree.cpp:170-185)
 //   k_voi            volume of interest per primitive           (linear_tree.cpp:216-283)
 //   k_camera         pixel rays, tile cones, superblock cones   (camera.cpp:29-37, abuffer.cpp:117-149)
-//   k_pairs          (volume, superblock) coarse cull           (superset of abuffer.cpp:193-196)
-//   k_tiles          exact tile cone + pixel pyramid per tile   (abuffer.cpp:193-196)
-//   k_raster         64 exact pixel-ray intervals per item      (abuffer.cpp:198-222)
-//   k_scan           tile counts -> CSR offsets (single pass)
-//   k_scatter        unsorted pool -> CSR slots
-//   k_sort           per-tile rank sort by (zEntry, word)       (insert_sorted, abuffer.cpp:166-173)
+//   k_pairs          (volume, superblock) coarse cull           (superset of abuffer.cpp:193-196),
+//                    counted per superblock
+//   k_scan           single-pass exclusive scan (superblock pair counts; tile
+//                    fragment counts for a CSR download)
+//   k_sb_scatter     pairs -> per-superblock candidate lists
+// The per-tile work -- the exact tile cone and pixel pyramid culls, the 64
+// exact ray intervals per candidate, the sorted fragment list -- is one warp
+// per tile in k_tile.cu.
 //
 // Everything on the A-buffer path is evaluated with ExactOps (no FMA, IEEE
 // div/sqrt), so (tile, word) membership and (zEntry, zExit) are bit-exact
 // with the reference's single-threaded rasterize_volumes.
 #include <algorithm>
 
-#include "bt_device.h"
+#include "bt_cull.cuh"
 
 namespace btk {
 
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kScanBlock = 4096;  // tiles per scan block (1024 threads x 4)
+constexpr uint32_t kScanBlock = kScanBlockElems;  // per scan block (1024 threads x 4)
 
 // ---------------------------------------------------------------- (a)
 
@@ -114,71 +116,6 @@ __device__ void pixel_pyramid(const Cam& c, int x0, int y0, int x1, int y1, floa
         }
         out[e] = make_float4(n.x, n.y, n.z, 0.0f);
     }
-}
-
-// Conservative volume-vs-pyramid test with a relative + absolute pad that
-// dominates every FP32 rounding on both sides.  Oriented boxes and capsules
-// use their own support along each inward plane normal, not their bounding
-// sphere's (19 % fewer (tile, volume) pairs to ray-test at C3).
-// A box (centre c, half-axis vectors A_i = h_i rotate(q, e_i); q is a unit
-// quaternion to 1e-6, validate_primitive) reaches n.(c - apex) + sum |n.A_i|;
-// a capsule max(n.(a - apex), n.(b - apex)) + r.  Same relative + absolute pad
-// as the sphere test, plus for capsules the cancellation error of the exact
-// capsule quadratic (~ulp(dist^2) / r in distance).  A pixel ray that the
-// exact test intersects lies inside the pyramid, so the volume reaches every
-// plane: a rejected (tile, volume) pair cannot produce a fragment.
-struct VolumeSupport {
-    uint32_t family;
-    F3 c, a0, a1, a2;  // box: centre, half-axis vectors; capsule: a0, a1 = ends
-    float r, pad;
-};
-
-__device__ __forceinline__ VolumeSupport volume_support(const Voi& v, F3 apex) {
-    VolumeSupport s;
-    s.family = v.family;
-    const Sphere bs = bounding_sphere(v);
-    const float vx = bs.c.x - apex.x, vy = bs.c.y - apex.y, vz = bs.c.z - apex.z;
-    const float dist = sqrtf(vx * vx + vy * vy + vz * vz);
-    s.pad = 1e-4f * (dist + fabsf(bs.r)) + 1e-5f;
-    if (v.family == 1u) {
-        const float w = v.rot.w, x = v.rot.x, y = v.rot.y, z = v.rot.z;
-        // columns of the rotation matrix of q, scaled by the half extents
-        s.a0 = F3{(1.f - 2.f * (y * y + z * z)) * v.half.x, 2.f * (x * y + w * z) * v.half.x, 2.f * (x * z - w * y) * v.half.x};
-        s.a1 = F3{2.f * (x * y - w * z) * v.half.y, (1.f - 2.f * (x * x + z * z)) * v.half.y, 2.f * (y * z + w * x) * v.half.y};
-        s.a2 = F3{2.f * (x * z + w * y) * v.half.z, 2.f * (y * z - w * x) * v.half.z, (1.f - 2.f * (x * x + y * y)) * v.half.z};
-        s.c = v.center;
-        s.r = 0.0f;
-    } else if (v.family == 2u) {
-        s.a0 = v.center;
-        s.a1 = v.axisEnd;
-        s.r = v.radius;
-        s.pad += 2.5e-7f * dist * dist / fmaxf(v.radius, 1e-6f);
-    } else {
-        s.c = bs.c;
-        s.r = bs.r;
-    }
-    return s;
-}
-
-__device__ __forceinline__ bool volume_pyramid_may_touch(const float4* pl, F3 apex, const VolumeSupport& s) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const float4 n = pl[e];
-        float reach;
-        if (s.family == 1u) {
-            reach = n.x * (s.c.x - apex.x) + n.y * (s.c.y - apex.y) + n.z * (s.c.z - apex.z) +
-                    fabsf(n.x * s.a0.x + n.y * s.a0.y + n.z * s.a0.z) +
-                    fabsf(n.x * s.a1.x + n.y * s.a1.y + n.z * s.a1.z) +
-                    fabsf(n.x * s.a2.x + n.y * s.a2.y + n.z * s.a2.z);
-        } else if (s.family == 2u) {
-            reach = fmaxf(n.x * (s.a0.x - apex.x) + n.y * (s.a0.y - apex.y) + n.z * (s.a0.z - apex.z),
-                          n.x * (s.a1.x - apex.x) + n.y * (s.a1.y - apex.y) + n.z * (s.a1.z - apex.z)) + s.r;
-        } else {
-            reach = n.x * (s.c.x - apex.x) + n.y * (s.c.y - apex.y) + n.z * (s.c.z - apex.z) + s.r;
-        }
-        if (reach < -s.pad) return false;
-    }
-    return true;
 }
 
 #ifndef BT_RASTER_MINB
@@ -362,170 +299,62 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
         uint32_t slot = 0;
         if (lane == 0) slot = atomicAdd(&fb.counters[kCntPairs], (uint32_t)__popc(m));
         slot = __shfl_sync(kFull, slot, 0) + __popc(m & ((1u << lane) - 1u));
-        if (pass && slot < fb.pairCap) fb.pairs[slot] = make_uint2(warp, (uint32_t)sb);
-    }
-}
-
-// One warp per (volume, superblock) pair, grid-stride: every lane tests two of
-// the superblock's 64 tiles with the exact reference cone (abuffer.cpp:193-196)
-// and the tile's pixel-centre pyramid; surviving (tile, volume) items are
-// appended with ONE warp-aggregated atomic per pair.
-__global__ void __launch_bounds__(256) k_tiles(Cam cam, const Voi* vois, FrameBufs fb, int tilesX, int tilesY,
-                                                uint32_t tile0, uint32_t tile1) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t npairs = min((uint64_t)fb.counters[kCntPairs], fb.pairCap);
-    const int sbX = (tilesX + kSB - 1) / kSB;
-    for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npairs; p += nwarps) {
-        const uint2 pr = fb.pairs[p];
-        const Voi vol = vois[pr.x];
-        const Sphere bs = bounding_sphere(vol);
-        const VolumeSupport sup = volume_support(vol, cam.pos);
-        const int sx = pr.y % sbX, sy = pr.y / sbX;
-        bool pass[2];
-        uint32_t tiles[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int lt = lane + 32 * h;
-            const int tx = sx * kSB + (lt & 7), ty = sy * kSB + (lt >> 3);
-            pass[h] = false;
-            tiles[h] = (uint32_t)(ty * tilesX + tx);
-            if (tx < tilesX && ty < tilesY && tiles[h] >= tile0 && tiles[h] < tile1) {
-                const float4 c = fb.cones[tiles[h]];
-                Cone k;
-                k.axis = F3{c.x, c.y, c.z};
-                k.cosH = c.w;
-                k.sinH = fb.coneSin[tiles[h]];
-                pass[h] = cone_may_touch(k, cam.pos, bs) &&
-                          volume_pyramid_may_touch(fb.tileFrustum + (size_t)tiles[h] * 4, cam.pos, sup);
-            }
-        }
-        const uint32_t m0 = __ballot_sync(kFull, pass[0]), m1 = __ballot_sync(kFull, pass[1]);
-        const uint32_t n = __popc(m0) + __popc(m1);
-        if (n == 0) continue;
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&fb.counters[kCntPool], n);
-        base = __shfl_sync(kFull, base, 0);
-        const uint32_t below = (1u << lane) - 1u;
-        if (pass[0]) {
-            const uint32_t slot = base + __popc(m0 & below);
-            if (slot < fb.poolCap) fb.pool[slot] = make_uint4(tiles[0], pr.x, 0u, 0u);
-        }
-        if (pass[1]) {
-            const uint32_t slot = base + __popc(m0) + __popc(m1 & below);
-            if (slot < fb.poolCap) fb.pool[slot] = make_uint4(tiles[1], pr.x, 0u, 0u);
+        if (pass && slot < fb.pairCap) {
+            fb.pairs[slot] = make_uint2(warp, (uint32_t)sb);
+            atomicAdd(&fb.sbCount[sb], 1u);  // lanes of a warp hold distinct superblocks
         }
     }
 }
 
-constexpr uint32_t kNoFragment = 0xFFFFFFFFu;
+// Single-pass exclusive scan of n counts: every 1024-thread block scans 4096
+// counts locally and publishes its sum; the last block to finish scans the
+// block sums.  offset(i) = local[i] + blockPrefix[i / 4096]; the total is
+// blockPrefix[nblocks].
+struct ScanArgs {
+    const uint32_t* count;
+    uint32_t* local;
+    uint32_t* blockSum;
+    uint32_t* blockPrefix;
+    uint32_t* done;
+};
 
-// One warp per (tile, volume) item, grid-stride: the tile's 64 pixel rays (two
-// per lane) are intersected with the volume exactly (abuffer.cpp:200-216),
-// clipped to [near, far], mapped to NDC and reduced with min/max (order-free
-// on these finite values).  The fragment lands in the item's own slot, so no
-// global append counter is contended; misses mark the slot empty.
-__global__ void __launch_bounds__(256, BT_RASTER_MINB) k_raster(Cam cam, const Voi* vois, FrameBufs fb) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t nitems = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
-    for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems; it += nwarps) {
-        const uint4 item = fb.pool[it];
-        const uint32_t tile = item.x;
-        const Voi v = vois[item.y];
-        const int tilesX = (cam.width + kTile - 1) / kTile;
-        const int tx = (int)(tile % (uint32_t)tilesX), ty = (int)(tile / (uint32_t)tilesX);
-        F3 ol{0.f, 0.f, 0.f};
-        if (v.family == 1u) ol = qrotate<E>(qconj(v.rot), vsub<E>(cam.pos, v.center));
-        float entry = f_inf(), exitv = -f_inf();
-        bool any = false;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int pix = lane + 32 * h;
-            const int px = tx * kTile + (pix & 7), py = ty * kTile + (pix >> 3);
-            if (px >= cam.width || py >= cam.height) continue;
-            const float4 rd = fb.rays[(size_t)tile * 64 + pix];
-            const F3 d{rd.x, rd.y, rd.z};
-            float t0, t1;
-            bool hit;
-            if (v.family == 0u)
-                hit = ray_sphere(cam.pos, d, v.center, v.radius, t0, t1);
-            else if (v.family == 1u)
-                hit = ray_obb_local(ol, d, v.rot, v.half, t0, t1);
-            else
-                hit = ray_capsule(cam.pos, d, v.center, v.axisEnd, v.radius, t0, t1);
-            if (!hit) continue;
-            float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
-            if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
-            vz0 = smax(vz0, cam.nearZ);
-            vz1 = smin(vz1, cam.farZ);
-            entry = smin(entry, vz0);  // view z for now: NDC is applied once per item below
-            exitv = smax(exitv, vz1);
-            any = true;
-        }
-        if (!__any_sync(kFull, any)) {
-            if (lane == 0) fb.pool[it].x = kNoFragment;
-            continue;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
-            exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
-        }
-        // ndc_from_view_z is monotone non-decreasing in vz (correctly rounded
-        // 1/vz, subtraction and scaling are each monotone), so the min / max
-        // over the rays of ndc(vz) is ndc of the min / max vz -- bit for bit
-        // the reference's per-ray min/max (abuffer.cpp:206-213), with two
-        // divisions per item instead of two per ray.
-        entry = ndc_from_view_z(cam, entry);
-        exitv = ndc_from_view_z(cam, exitv);
-        if (lane == 0) {
-            fb.pool[it] = make_uint4(tile, item.y, __float_as_uint(entry), __float_as_uint(exitv));
-            atomicAdd(&fb.tileCount[tile], 1u);
-        }
-    }
-}
-
-// Single-pass scan: every 1024-thread block scans 4096 tile counts locally
-// and publishes its sum; the last block to finish scans the block sums.
-// offset(tile) = tileLocal[tile] + blockPrefix[tile / 4096].
-__global__ void __launch_bounds__(1024) k_scan(FrameBufs fb, uint32_t tiles) {
+__global__ void __launch_bounds__(1024) k_scan(ScanArgs a, uint32_t n) {
     __shared__ uint32_t warpSums[32];
     __shared__ bool amLast;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t base = blockIdx.x * kScanBlock + tid * 4;
     uint32_t v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (base + k < tiles) ? fb.tileCount[base + k] : 0u;
+    for (int k = 0; k < 4; ++k) v[k] = (base + k < n) ? a.count[base + k] : 0u;
     const uint32_t local = v[0] + v[1] + v[2] + v[3];
     uint32_t incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t n = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += n;
+        const uint32_t nb = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += nb;
     }
     if (lane == 31) warpSums[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        uint32_t s = warpSums[lane];
+        uint32_t sm = warpSums[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t n = __shfl_up_sync(kFull, s, o);
-            if (lane >= o) s += n;
+            const uint32_t nb = __shfl_up_sync(kFull, sm, o);
+            if (lane >= o) sm += nb;
         }
-        warpSums[lane] = s;  // inclusive
+        warpSums[lane] = sm;  // inclusive
     }
     __syncthreads();
     uint32_t run = incl - local + (wid > 0 ? warpSums[wid - 1] : 0u);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        if (base + k < tiles) fb.tileLocal[base + k] = run;
+        if (base + k < n) a.local[base + k] = run;
         run += v[k];
     }
     if (tid == 0) {
-        fb.blockSum[blockIdx.x] = warpSums[31];
+        a.blockSum[blockIdx.x] = warpSums[31];
         __threadfence();
-        const uint32_t done = atomicAdd(&fb.counters[kCntScanDone], 1u);
+        const uint32_t done = atomicAdd(a.done, 1u);
         amLast = (done == gridDim.x - 1);
     }
     __syncthreads();
@@ -534,104 +363,66 @@ __global__ void __launch_bounds__(1024) k_scan(FrameBufs fb, uint32_t tiles) {
         uint32_t carry = 0;
         for (uint32_t b0 = 0; b0 < gridDim.x; b0 += 32) {
             const uint32_t b = b0 + lane;
-            const uint32_t s = b < gridDim.x ? *((volatile uint32_t*)&fb.blockSum[b]) : 0u;
-            uint32_t inc = s;
+            const uint32_t sv = b < gridDim.x ? *((volatile uint32_t*)&a.blockSum[b]) : 0u;
+            uint32_t inc = sv;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t n = __shfl_up_sync(kFull, inc, o);
-                if (lane >= o) inc += n;
+                const uint32_t nb = __shfl_up_sync(kFull, inc, o);
+                if (lane >= o) inc += nb;
             }
-            if (b < gridDim.x) fb.blockPrefix[b] = carry + inc - s;
+            if (b < gridDim.x) a.blockPrefix[b] = carry + inc - sv;
             carry += __shfl_sync(kFull, inc, 31);
         }
-        if (lane == 0) fb.blockPrefix[gridDim.x] = carry;
-    }
-}
-
-__device__ __forceinline__ uint32_t tile_offset(const FrameBufs& fb, uint32_t tile) {
-    return fb.tileLocal[tile] + fb.blockPrefix[tile / kScanBlock];
-}
-
-// true when this frame's fragments do not fit the pool (the host grows the
-// buffers and rebuilds; in a graph replay the A-buffer degrades to empty)
-__device__ __forceinline__ bool pool_overflowed(const FrameBufs& fb) {
-    return (uint64_t)fb.counters[kCntPool] > fb.poolCap || (uint64_t)fb.counters[kCntPairs] > fb.pairCap;
-}
-
-__global__ void k_scatter(const Voi* vois, FrameBufs fb) {
-    if (pool_overflowed(fb)) return;
-    const uint32_t n = min((uint64_t)fb.counters[kCntPool], fb.poolCap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint4 r = fb.pool[i];
-        if (r.x == kNoFragment) continue;
-        const uint32_t slot = tile_offset(fb, r.x) + atomicAdd(&fb.tileCursor[r.x], 1u);
-        fb.unsorted[slot] = make_uint4(vois[r.y].word, r.z, r.w, r.y);
-    }
-}
-
-// key order of insert_sorted: (zEntry, word); equal keys keep volume order
-// (upper_bound insertion in volume order), hence the volume index tiebreak.
-__device__ __forceinline__ bool key_less(const uint4& a, const uint4& b) {
-    const float ea = __uint_as_float(a.y), eb = __uint_as_float(b.y);
-    if (ea != eb) return ea < eb;
-    if (a.x != b.x) return a.x < b.x;
-    return a.w < b.w;
-}
-
-constexpr int kSortStage = 256;
-
-// Warp per tile of [first, last) (the frame's tile range).
-__global__ void __launch_bounds__(128) k_sort(FrameBufs fb, uint32_t tiles, uint32_t first, uint32_t last) {
-    __shared__ uint4 stage[4][kSortStage];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = first + blockIdx.x * 4 + wid;
-    if (tile >= last) return;
-    if (pool_overflowed(fb)) {  // never index past the pool: empty A-buffer, flagged
         if (lane == 0) {
-            fb.offsets[tile] = 0;
-            if (tile == tiles - 1) fb.offsets[tiles] = 0;
-            if (tile == first) atomicExch(&fb.counters[kCntOverflow], 1u);
+            a.blockPrefix[gridDim.x] = carry;
+            *a.done = 0u;  // ready for the next scan on this counter
         }
-        return;
-    }
-    const uint32_t n = fb.tileCount[tile];
-    const uint32_t off = tile_offset(fb, tile);
-    fb.offsets[tile] = off;
-    if (tile == tiles - 1 && lane == 0) fb.offsets[tiles] = off + n;
-    if (n == 0) return;
-    const uint4* src = fb.unsorted + off;
-    const bool staged = n <= (uint32_t)kSortStage;
-    if (staged)
-        for (uint32_t i = lane; i < n; i += 32) stage[wid][i] = src[i];
-    __syncwarp();
-    const uint4* keys = staged ? stage[wid] : src;
-    for (uint32_t i = lane; i < n; i += 32) {
-        const uint4 me = keys[i];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < n; ++j) rank += key_less(keys[j], me) ? 1u : 0u;
-        Frag f;
-        f.word = me.x;
-        f.zEntry = __uint_as_float(me.y);
-        f.zExit = __uint_as_float(me.z);
-        fb.frags[off + rank] = f;
     }
 }
 
-// CSR offsets of every tile, thread per tile: a sharded frame sorts only its
-// own tile range, the other tiles are empty but keep valid offsets.
-__global__ void k_offsets_all(FrameBufs fb, uint32_t tiles) {
+__device__ __forceinline__ uint32_t sb_offset(const FrameBufs& fb, uint32_t sb) {
+    return fb.sbLocal[sb] + fb.sbBlockPrefix[sb / kScanBlock];
+}
+
+// (volume, superblock) pairs -> per-superblock candidate lists (list order is
+// free: a tile's fragments are sorted by (zEntry, word, volume) afterwards)
+__global__ void k_sb_scatter(FrameBufs fb) {
+    if ((uint64_t)fb.counters[kCntPairs] > fb.pairCap) return;  // overflow: k_tile flags the frame
+    const uint32_t n = fb.counters[kCntPairs];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint2 pr = fb.pairs[i];
+        fb.sbList[sb_offset(fb, pr.y) + atomicAdd(&fb.sbCursor[pr.y], 1u)] = pr.x;
+    }
+}
+
+// --- CSR of the A-buffer for a download (the frame itself never needs it)
+__global__ void k_frag_counts(FrameBufs fb, uint32_t tiles) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= tiles) return;
-    const bool ov = pool_overflowed(fb);
-    const uint32_t off = ov ? 0u : tile_offset(fb, t);
-    fb.offsets[t] = off;
-    if (t == tiles - 1) fb.offsets[tiles] = ov ? 0u : off + fb.tileCount[t];
+    if (t < tiles) fb.tileCount[t] = fb.tileFrag[t].y;
 }
 
-__global__ void k_offsets_from_counts(FrameBufs fb, uint32_t tiles) {
-    // used when the A-buffer was uploaded: counts from CSR offsets
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < tiles) fb.tileCount[i] = fb.offsets[i + 1] - fb.offsets[i];
+__global__ void k_frag_offsets(FrameBufs fb, uint32_t tiles) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > tiles) return;
+    fb.offsets[t] = t < tiles ? fb.tileLocal[t] + fb.blockPrefix[t / kScanBlock]
+                              : fb.blockPrefix[(tiles + kScanBlock - 1) / kScanBlock];
+}
+
+// warp per tile: the tile's sorted list -> its CSR slots (fb.unsorted as Frag)
+__global__ void k_frag_copy(FrameBufs fb, uint32_t tiles) {
+    const uint32_t lane = threadIdx.x & 31u;
+    Frag* csr = reinterpret_cast<Frag*>(fb.unsorted);
+    for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles; t += (gridDim.x * blockDim.x) >> 5) {
+        const uint2 tf = fb.tileFrag[t];
+        const uint32_t o = fb.offsets[t];
+        for (uint32_t i = lane; i < tf.y; i += 32) csr[o + i] = fb.frags[tf.x + i];
+    }
+}
+
+// an uploaded CSR A-buffer: every tile's list is its CSR range
+__global__ void k_tile_frag_from_offsets(FrameBufs fb, uint32_t tiles) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tiles) fb.tileFrag[t] = make_uint2(fb.offsets[t], fb.offsets[t + 1] - fb.offsets[t]);
 }
 
 }  // namespace
@@ -684,14 +475,20 @@ void launch_camera(cudaStream_t st, const Cam& cam, const FrameBufs& fb, int til
     if (sbHi > sbLo) k_camera<<<sbHi - sbLo, 256, 0, st>>>(cam, fb, tilesX, tilesY, sbLo);
 }
 
+uint32_t superblock_count(int tilesX, int tilesY) {
+    return (uint32_t)(((tilesX + kSB - 1) / kSB) * ((tilesY + kSB - 1) / kSB));
+}
+
+// Superblock stage of the A-buffer: (volume, superblock) pairs, grouped by
+// superblock.  The per-tile stage is launch_tile_pass (k_tile.cu).
 void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t nvoi,
                     const FrameBufs& fb, int tilesX, int tilesY, uint32_t tile0, uint32_t tile1,
                     int smCount, bool zero) {
-    const uint32_t tiles = (uint32_t)(tilesX * tilesY);
+    const uint32_t nsbAll = superblock_count(tilesX, tilesY);
     if (zero) {
         cudaMemsetAsync(fb.counters, 0, kCntSlots * sizeof(uint32_t), st);
-        cudaMemsetAsync(fb.tileCount, 0, tiles * sizeof(uint32_t), st);
-        cudaMemsetAsync(fb.tileCursor, 0, tiles * sizeof(uint32_t), st);
+        cudaMemsetAsync(fb.sbCount, 0, nsbAll * sizeof(uint32_t), st);
+        cudaMemsetAsync(fb.sbCursor, 0, nsbAll * sizeof(uint32_t), st);
     }
     if (nvoi > 0) {
         int sbLo, sbHi;
@@ -704,23 +501,22 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
             std::max<uint32_t>(1u, std::min<uint32_t>((nsb + 31) / 32, std::max<uint32_t>(1u, 2048u / nvoi)));
         const dim3 grid((nvoi * 32 + 255) / 256, chunks);
         k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1, sbLo, sbHi);
-        k_tiles<<<smCount * 8, 256, 0, st>>>(cam, vois, fb, tilesX, tilesY, tile0, tile1);
-        k_raster<<<smCount * 8, 256, 0, st>>>(cam, vois, fb);
     }
-    const uint32_t nblocks = (tiles + kScanBlock - 1) / kScanBlock;
-    k_scan<<<nblocks, 1024, 0, st>>>(fb, tiles);
-    k_scatter<<<smCount * 4, 256, 0, st>>>(vois, fb);
-    if (tile0 == 0 && tile1 >= tiles) {
-        k_sort<<<(tiles + 3) / 4, 128, 0, st>>>(fb, tiles, 0u, tiles);
-    } else {
-        k_offsets_all<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
-        const uint32_t last = std::min(tile1, tiles);
-        if (last > tile0) k_sort<<<(last - tile0 + 3) / 4, 128, 0, st>>>(fb, tiles, tile0, last);
-    }
+    ScanArgs a{fb.sbCount, fb.sbLocal, fb.sbBlockSum, fb.sbBlockPrefix, fb.counters + kCntScanDone2};
+    k_scan<<<(nsbAll + kScanBlock - 1) / kScanBlock, 1024, 0, st>>>(a, nsbAll);
+    if (nvoi > 0) k_sb_scatter<<<smCount * 2, 256, 0, st>>>(fb);
 }
 
-void launch_offsets_from_counts(cudaStream_t st, const FrameBufs& fb, uint32_t tiles) {
-    k_offsets_from_counts<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
+void launch_frag_csr(cudaStream_t st, const FrameBufs& fb, uint32_t tiles, int smCount) {
+    k_frag_counts<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
+    ScanArgs a{fb.tileCount, fb.tileLocal, fb.blockSum, fb.blockPrefix, fb.counters + kCntScanDone};
+    k_scan<<<(tiles + kScanBlock - 1) / kScanBlock, 1024, 0, st>>>(a, tiles);
+    k_frag_offsets<<<(tiles + 256) / 256, 256, 0, st>>>(fb, tiles);
+    k_frag_copy<<<smCount * 4, 256, 0, st>>>(fb, tiles);
+}
+
+void launch_tile_frag_from_offsets(cudaStream_t st, const FrameBufs& fb, uint32_t tiles) {
+    k_tile_frag_from_offsets<<<(tiles + 255) / 256, 256, 0, st>>>(fb, tiles);
 }
 
 }  // namespace btk

@@ -154,7 +154,7 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
 #endif
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
-        if constexpr (Cls == kClsSingle) v = fast_prim(uaux & 7u, s.blocks + (uaux >> 3), p);
+        if constexpr (Cls == kClsSingle) v = fast_prim(comb_rec_kind(uaux), s.blocks + (uaux >> 5), p);
         else if constexpr (Cls == kClsComb) v = eval_comb(s.rec, uaux, s.blocks, p);
         else if constexpr (Cls == kClsGeneral) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
         else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);  // exact path, or an oversized view

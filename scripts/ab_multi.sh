@@ -7,7 +7,7 @@ for round in 1 2 3; do
   for v in ${VARS:-A B}; do
     cp paper_2304_09673_b200/lib/ab/lib$v.so $LIB
     for cfg in ${CFGS:-C3 C5 C1}; do
-      echo "$v $cfg $(timeout 100 python scripts/march_bench.py $cfg 40 2>&1 | tail -1 | awk '{print $3, $5, $7}')"
+      echo "$v $cfg $(timeout 100 python ${BENCH:-scripts/march_bench.py} $cfg 40 2>&1 | tail -1)"
     done
   done
 done
