@@ -21,8 +21,10 @@ synchronized sphere tracing -> normals, replayed from one CUDA graph.
               cores on one C3 frame.
 --impl reference times that reference CPU path per step instead.
 Multi-GPU (torchrun): the frame's tile rows are split over ranks (strong
-scaling); each rank traces its rows and rank 0 gathers hit/depth/evalCount
-with NCCL.
+scaling); each rank traces its rows straight into rank 0's G-buffer over
+peer memory (fused gather, CUDA IPC; NCCL gather as the fallback) and shades
+its own rows' normals there.  Beside the C3 headline every run also times
+the C4 scaling config (scaling_c4).
 """
 from __future__ import annotations
 
@@ -204,13 +206,144 @@ def run_reference(args, rank: int):
 
 # ---------------------------------------------------------------------------- B200 arm
 
+class ShardedFrames:
+    """One rank's share of the frame sequence of a config: the scene, its
+    renderer on this rank's stream, the per-frame parameter deltas resident
+    in HBM, the rank's tile rows, and the exchange with the other ranks.
+
+    Multi-GPU exchange.  Preferred: the fused gather -- rank 0 exports its
+    G-buffer planes (CUDA IPC), the other ranks import them, so every march
+    writes its rows straight into rank 0's G-buffer over NVLink while it
+    runs; a one-element all-reduce on the stream then orders every rank's
+    normals (its own rows, the one-row depth halo read from rank 0's planes,
+    written into rank 0's normal plane) after every rank's march, and a
+    second one orders the next frame's peer writes after every rank's
+    normals.  Fallback: NCCL gather of the rows, normals on rank 0."""
+
+    def __init__(self, config, args, rank, world, dev, stream, frames):
+        import ctypes as C
+
+        import torch
+
+        from paper_2304_09673_b200 import _capi as capi
+        from paper_2304_09673_b200.distributed import tile_row_ranges
+        from paper_2304_09673_b200.pipeline import RenderConfig, Renderer, Scene
+        self.rank, self.world, self.dev = rank, world, dev
+        self.scene = Scene.build(config)
+        self.rd = Renderer(dev.index)
+        self.rd.set_stream(stream.cuda_stream)
+        self.rd.upload(self.scene)
+        self.lib = self.rd.lib
+        self.cam = self.scene.device_camera
+        self.cfg = RenderConfig()
+        self.exact = bool(args.exact)
+        self.W, self.H = self.scene.width, self.scene.height
+        tiles_x, tiles_y = self.scene.tiles
+        # strong scaling: contiguous tile-row ranges per rank
+        self.rows = tile_row_ranges(tiles_y, world)
+        self.tile0, self.tile1 = int(self.rows[rank] * tiles_x), int(self.rows[rank + 1] * tiles_x)
+        if world == 1:
+            self.tile0, self.tile1 = 0, 0
+        # all frames' parameter deltas resident in HBM before timing
+        self.host_frames = [self.scene.perturb(f) for f in range(frames)]
+        self.nprim = len(self.scene.prims)
+        self.d_words = [torch.from_numpy(w.view(np.int32)).to(dev) for w, _, _ in self.host_frames]
+        self.d_params = [torch.from_numpy(p).to(dev) for _, p, _ in self.host_frames]
+        self.d_counts = [torch.from_numpy(c.view(np.int32)).to(dev) for _, _, c in self.host_frames]
+        self.planes = {}
+        self.fused = False
+        if world > 1:
+            import torch.distributed as dist
+            self.rd.render_frame(self.cam, self.cfg, exact=self.exact, graph=False, tile0=self.tile0,
+                                 tile1=self.tile1, normals=False)
+            torch.cuda.synchronize(dev)
+            ok = 1
+            h = capi.bt_ipc_handles()
+            if rank == 0 and self.lib.bt_gbuffer_export(self.rd.ctx, C.byref(h)) != 0:
+                ok = 0
+            obj = [bytes(h), ok]
+            dist.broadcast_object_list(obj, src=0)
+            if obj[1] and rank != 0:
+                C.memmove(C.addressof(h), obj[0], C.sizeof(h))
+                ok = 1 if self.lib.bt_gbuffer_import(self.rd.ctx, C.byref(h)) == 0 else 0
+            flag = torch.tensor([ok if obj[1] else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            self.fused = bool(flag.item())
+            if not self.fused and rank != 0:
+                self.lib.bt_gbuffer_import_release(self.rd.ctx)
+            self.done = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def render(self, f):
+        """frame f up to a complete G-buffer on rank 0 (device-resident deltas)"""
+        rd, world = self.rd, self.world
+        rd.update_params_device(self.d_words[f].data_ptr(), self.d_params[f].data_ptr(), self.d_counts[f].data_ptr(),
+                                self.nprim)
+        self.render_rows()
+
+    def render_rows(self):
+        from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes
+        rd, world = self.rd, self.world
+        rd.render_frame(self.cam, self.cfg, exact=self.exact, graph=True, tile0=self.tile0, tile1=self.tile1,
+                        normals=(world == 1))
+        if world == 1:
+            return
+        import torch.distributed as dist
+        if self.fused:
+            dist.all_reduce(self.done)  # stream-ordered: every rank's march has written its rows
+            rd.compute_normals_rows(self.cam, self.tile0, self.tile1, self.cfg.normalsMode, self.exact)
+            dist.all_reduce(self.done)  # every rank's normals are in: the frame is complete on rank 0
+        else:
+            # this rank's rows of hit/depth/evalCount -> rank 0 (NCCL), normals on rank 0
+            if not self.planes:
+                self.planes.update(gbuffer_planes(rd.gbuffer_device(), self.dev))
+            gather_rows(self.planes, self.rows, self.rank, world, self.W, self.H)
+            if self.rank == 0:
+                rd.compute_normals(self.cam, self.cfg.normalsMode, self.exact)
+
+    def release(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+            if self.fused and self.rank != 0:
+                self.lib.bt_gbuffer_import_release(self.rd.ctx)
+            dist.barrier()
+        self.rd.close()
+
+
+def device_ms(fr, args, stream, flush, f0=0):
+    """CUDA-event ms per frame over args.steps frames after args.warmup
+    untimed ones (L2 flushed between frames, untimed), max over ranks."""
+    import torch
+    dev = fr.dev
+    for f in range(args.warmup):
+        fr.render(f0 + f)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if fr.world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        fr.render(f0 + args.warmup + i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if fr.world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
 def run_b200(args, rank: int, world: int, local_rank: int):
     import ctypes as C
 
     import torch
 
     from paper_2304_09673_b200 import _capi as capi
-    from paper_2304_09673_b200.pipeline import RenderConfig, Renderer, Scene
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -220,76 +353,18 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_stream(stream)
     lib = capi.load()
 
-    scene = Scene.build(args.config)
-    rd = Renderer(local_rank)
-    rd.set_stream(stream.cuda_stream)
-    rd.upload(scene)
-    cam = scene.device_camera
-    cfg = RenderConfig()
-    exact = bool(args.exact)
-    W, H = scene.width, scene.height
-    tiles_x, tiles_y = scene.tiles
-    # strong scaling: contiguous tile-row ranges per rank
-    from paper_2304_09673_b200.distributed import tile_row_ranges
-    rows = tile_row_ranges(tiles_y, world)
-    tile0, tile1 = int(rows[rank] * tiles_x), int(rows[rank + 1] * tiles_x)
-    if world == 1:
-        tile0, tile1 = 0, 0
-
-    # all frames' parameter deltas resident in HBM before timing
     nframes = args.warmup + args.steps
-    host_frames = [scene.perturb(f) for f in range(nframes)]
-    nprim = len(scene.prims)
-    d_words = [torch.from_numpy(w.view(np.int32)).to(dev) for w, _, _ in host_frames]
-    d_params = [torch.from_numpy(p).to(dev) for _, p, _ in host_frames]
-    d_counts = [torch.from_numpy(c.view(np.int32)).to(dev) for _, _, c in host_frames]
+    fr = ShardedFrames(args.config, args, rank, world, dev, stream, nframes)
+    scene, rd, cam, cfg, exact = fr.scene, fr.rd, fr.cam, fr.cfg, fr.exact
+    W, H = fr.W, fr.H
+    tiles_x, tiles_y = scene.tiles
+    tile0, tile1, rows, fused, planes = fr.tile0, fr.tile1, fr.rows, fr.fused, fr.planes
+    host_frames, nprim = fr.host_frames, fr.nprim
+    d_words, d_params, d_counts = fr.d_words, fr.d_params, fr.d_counts
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes, tile_row_ranges
-    planes = {}
-
-    # Multi-GPU exchange.  Preferred: the fused gather -- rank 0 exports its
-    # G-buffer planes (CUDA IPC), the other ranks import them and their marches
-    # write their rows straight into rank 0's G-buffer over NVLink while they
-    # run; a one-element all-reduce on the stream then orders rank 0's normals
-    # after every rank's march.  Fallback: NCCL gather of the rows.
-    fused = False
-    if world > 1:
-        import ctypes as _C
-        import torch.distributed as dist
-        rd.render_frame(cam, cfg, exact=exact, graph=False, tile0=tile0, tile1=tile1, normals=False)
-        torch.cuda.synchronize(dev)
-        ok = 1
-        h = capi.bt_ipc_handles()
-        if rank == 0 and lib.bt_gbuffer_export(rd.ctx, _C.byref(h)) != 0:
-            ok = 0
-        obj = [bytes(h), ok]
-        dist.broadcast_object_list(obj, src=0)
-        if obj[1] and rank != 0:
-            _C.memmove(_C.addressof(h), obj[0], _C.sizeof(h))
-            ok = 1 if lib.bt_gbuffer_import(rd.ctx, _C.byref(h)) == 0 else 0
-        flag = torch.tensor([ok if obj[1] else 0], dtype=torch.int32, device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        fused = bool(flag.item())
-        if not fused and rank != 0:
-            lib.bt_gbuffer_import_release(rd.ctx)
-        done = torch.zeros(1, dtype=torch.int32, device=dev)
-
     def step(f):
-        rd.update_params_device(d_words[f].data_ptr(), d_params[f].data_ptr(), d_counts[f].data_ptr(), nprim)
-        rd.render_frame(cam, cfg, exact=exact, graph=True, tile0=tile0, tile1=tile1, normals=(world == 1))
-        if world > 1:
-            if fused:
-                dist.all_reduce(done)  # stream-ordered: every rank's march has written its rows
-            else:
-                # this rank's rows of hit/depth/evalCount -> rank 0 (NCCL)
-                if not planes:
-                    planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
-                gather_rows(planes, rows, rank, world, W, H)
-            if rank == 0:  # normals over the whole image (they need neighbour rows)
-                rd.compute_normals(cam, cfg.normalsMode, exact)
-            if fused:  # rank 0 has read every row: the next frame's peer writes may land
-                dist.all_reduce(done)
+        fr.render(f)
 
     for f in range(args.warmup):
         step(f)
@@ -332,8 +407,10 @@ def run_b200(args, rank: int, world: int, local_rank: int):
 
     e2e_multi = None
     if world > 1:
-        e2e_multi = e2e_pass_multi(rd, scene, cam, cfg, exact, host_frames, args, rank, world, tile0, tile1, fused,
-                                   planes, rows)
+        e2e_multi = e2e_pass_multi(fr, args)
+    scaling = None
+    if not args.no_sweep:  # the C4 scaling curve beside the headline, at every N
+        scaling = scaling_block("C4", args, rank, world, dev, stream, flush)
     if rank != 0:
         return
     result = {
@@ -350,6 +427,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "gpu_launches": launches,
         "clocks": {k: clock[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
     }
+    if scaling is not None:
+        result["scaling_c4"] = scaling
 
     # ------------------------------------------------------------------ per-stage + roofline (untimed pass)
     stage_ms, flops_per_frame, st = stage_breakdown(rd, cam, cfg, exact, d_words, d_params, d_counts, nprim)
@@ -382,10 +461,10 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     ab_bytes = nprim * 64 + tiles_x * tiles_y * 8 + st.fragments * 12
     ab_gbs = ab_bytes / (stage_ms["abuffer"] * 1e-3) / 1e9
     result["abuffer_roofline"] = {
-        "kernels": "k_pairs, k_tiles, k_raster, k_scan, k_scatter, k_sort", "bound": "hbm",
+        "kernels": "k_camera, k_pairs, k_scan, k_sb_scatter, k_tile_raster", "bound": "hbm",
         "achieved": round(ab_gbs, 2), "peak": hbm, "unit": "GB/s",
         "frac": round(ab_gbs / hbm, 5) if hbm else None, "algorithmic_bytes": ab_bytes,
-        "note": "latency/IEEE-division bound at these sizes: the algorithmic traffic is ~2 MB per frame",
+        "note": "bound by the exact IEEE ray tests (instruction issue), not HBM: the algorithmic traffic is ~2 MB per frame",
         "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-written)"}
     result["frame_stats"] = {"fieldEvals": st.fieldEvals, "warpSteps": st.warpSteps,
                              "laneUtilisation": round(st.fieldEvals / max(1, 32 * st.warpSteps), 4),
@@ -528,51 +607,41 @@ def e2e_pass(rd, scene, cam, cfg, exact, host_frames, args) -> dict:
                              "path": "same with the blocking bt_gbuffer_download per frame"}}
 
 
-def e2e_pass_multi(rd, scene, cam, cfg, exact, host_frames, args, rank, world, tile0, tile1, fused, planes,
-                   rows) -> dict | None:
+def e2e_pass_multi(fr, args) -> dict | None:
     """N GPUs end to end, wall clock, max over ranks: per step every rank
-    uploads the frame's parameter deltas from pinned host memory and traces
-    its tile rows into rank 0's G-buffer (fused gather, or the NCCL gather);
-    rank 0 computes the normals and streams the whole G-buffer into a pinned
-    host slab; every frame is on the host when the timed region ends."""
+    uploads the frame's parameter deltas from pinned host memory, traces its
+    tile rows into rank 0's G-buffer and shades their normals there (fused
+    gather; or the NCCL gather + normals on rank 0); rank 0 streams the whole
+    G-buffer into a pinned host slab; every frame is on the host when the
+    timed region ends."""
     import ctypes as C
 
     import torch
     import torch.distributed as dist
 
     from paper_2304_09673_b200 import _capi as capi
-    from paper_2304_09673_b200.distributed import gather_rows, gbuffer_planes
-    lib = rd.lib
-    dev = torch.device("cuda", torch.cuda.current_device())
-    W, H = scene.width, scene.height
-    n = len(scene.prims)
+    rd, lib, rank, world, dev = fr.rd, fr.lib, fr.rank, fr.world, fr.dev
+    W, H = fr.W, fr.H
+    n = fr.nprim
     pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
-    frames = [(pin(w.view(np.int32)), pin(p), pin(c.view(np.int32))) for w, p, c in host_frames]
+    frames = [(pin(w.view(np.int32)), pin(p), pin(c.view(np.int32))) for w, p, c in fr.host_frames]
     slabs = []
     if rank == 0:
         off = (C.c_size_t * 7)()
         total = C.c_size_t()
         capi.check(lib.bt_gbuffer_layout(rd.ctx, off, C.byref(total)), "bt_gbuffer_layout")
         slabs = [torch.empty(total.value, dtype=torch.uint8).pin_memory() for _ in range(2)]
-    done = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def step(f, i):
         w, p, c = frames[f]
         capi.check(lib.bt_params_update(rd.ctx, C.c_void_p(w.data_ptr()), C.c_void_p(p.data_ptr()),
                                         C.c_void_p(c.data_ptr()), n, 17), "bt_params_update")
-        rd.render_frame(cam, cfg, exact=exact, graph=True, tile0=tile0, tile1=tile1, normals=False)
-        if fused:
-            dist.all_reduce(done)
-        else:
-            if not planes:
-                planes.update(gbuffer_planes(rd.gbuffer_device(), dev))
-            gather_rows(planes, rows, rank, world, W, H)
+        fr.render_rows()
         if rank == 0:
-            rd.compute_normals(cam, cfg.normalsMode, exact)
             capi.check(lib.bt_gbuffer_download_async_slab(rd.ctx, C.c_void_p(slabs[i % 2].data_ptr())),
                        "bt_gbuffer_download_async_slab")
-        if fused:  # the snapshot is taken: the next frame's peer writes may land
-            dist.all_reduce(done)
+        if fr.fused:  # the snapshot is taken: the next frame's peer writes may land
+            dist.all_reduce(fr.done)
 
     for i in range(args.warmup):
         step(i, i)
@@ -589,13 +658,29 @@ def e2e_pass_multi(rd, scene, cam, cfg, exact, host_frames, args, rank, world, t
     dt = torch.tensor([(time.perf_counter() - t0) / args.steps], device=dev)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     dt = float(dt.item())
-    tx, ty = scene.tiles
+    tx, ty = fr.scene.tiles
     return {"value": round(W * H / dt / 1e6, 2), "unit": "Mrays/s", "ms_per_step": round(dt * 1e3, 4),
             "h2d_bytes_per_step": world * n * (4 + 17 * 4 + 4),
             "d2h_bytes_per_step": W * H * (1 + 4 + 12 + 4) + tx * ty * (4 + 4 + 1),
-            "path": "every rank: bt_params_update (pinned host) -> bt_render_frame (its tile rows, "
-                    f"{'fused gather into rank 0' if fused else 'NCCL gather to rank 0'}); rank 0: bt_normals -> "
-                    "bt_gbuffer_download_async_slab (pinned host); wall clock, max over ranks"}
+            "path": "every rank: bt_params_update (pinned host) -> bt_render_frame (its tile rows) -> "
+                    + ("bt_normals_rows (its rows, into rank 0's planes over peer memory)" if fr.fused else
+                       "NCCL gather to rank 0 -> bt_normals on rank 0")
+                    + "; rank 0: bt_gbuffer_download_async_slab (pinned host); wall clock, max over ranks"}
+
+
+def scaling_block(config, args, rank, world, dev, stream, flush) -> dict:
+    """The multi-GPU scaling config (C4, 10,000 primitives at
+    3840x2160) timed the same way as the headline at this N (device time,
+    max over ranks), so the driver's N = 1, 2, 4, 8 runs carry a C4 curve
+    beside the C3 one."""
+    fr = ShardedFrames(config, args, rank, world, dev, stream, args.warmup + args.steps)
+    ms = device_ms(fr, args, stream, flush)
+    out = {"config": config, "n_gpus": world, "ms_per_frame": round(ms, 4),
+           "Mrays_s": round(fr.W * fr.H / (ms * 1e-3) / 1e6, 1),
+           "exchange": ("fused gather + per-rank normals over peer memory" if fr.fused else "NCCL gather")
+           if world > 1 else "none"}
+    fr.release()
+    return out
 
 
 def eager_stages(r, cam, cfg, exact, frames: int = 3) -> dict:

@@ -201,6 +201,14 @@ BT_API int bt_abuffer_upload(bt_ctx* ctx, const bt_camera* cam, const uint32_t* 
 BT_API int bt_trace(bt_ctx* ctx, const bt_camera* cam, const bt_render_config* cfg,
                     uint32_t tile0, uint32_t tile1, int exact);
 BT_API int bt_normals(bt_ctx* ctx, const bt_camera* cam, int mode, int exact);
+/* compute_normals (tracer.cpp:296-350) for the pixels of the tile rows
+ * covering [tile0, tile1) only: a sharded rank shades its own rows.  With an
+ * imported G-buffer (bt_gbuffer_import) the depths -- its rows and the
+ * neighbour rows of the halo -- are read from, and the normals written to,
+ * the root's planes over peer memory; the gradient fallback uses this
+ * context's own interval records and tree.  Every rank's trace must be
+ * complete (e.g. a stream-ordered collective) before any rank calls it. */
+BT_API int bt_normals_rows(bt_ctx* ctx, const bt_camera* cam, int mode, int exact, uint32_t tile0, uint32_t tile1);
 BT_API int bt_oracle_render(bt_ctx* ctx, const bt_camera* cam, const bt_render_config* cfg,
                             int exact);
 
@@ -248,7 +256,7 @@ BT_API int bt_gbuffer_download_async_slab(bt_ctx* ctx, void* slab);
  * After the ranks' streams are done (a host barrier), the root computes the
  * normals of the assembled frame. */
 typedef struct bt_ipc_handles {
-    unsigned char plane[6][64]; /* hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError */
+    unsigned char plane[7][64]; /* hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError, normal */
     int32_t width, height;
 } bt_ipc_handles;
 BT_API int bt_gbuffer_export(bt_ctx* ctx, bt_ipc_handles* out);

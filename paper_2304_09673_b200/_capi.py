@@ -49,7 +49,7 @@ class bt_fragment(C.Structure):
 
 
 class bt_ipc_handles(C.Structure):
-    _fields_ = [("plane", (C.c_ubyte * 64) * 6), ("width", C.c_int32), ("height", C.c_int32)]
+    _fields_ = [("plane", (C.c_ubyte * 64) * 7), ("width", C.c_int32), ("height", C.c_int32)]
 
 
 class bt_stats(C.Structure):
@@ -94,6 +94,7 @@ PROTOTYPES = {
     "bt_abuffer_upload": [vp, P(bt_camera), vp, vp],
     "bt_trace": [vp, P(bt_camera), P(bt_render_config), u32, u32, C.c_int],
     "bt_normals": [vp, P(bt_camera), C.c_int, C.c_int],
+    "bt_normals_rows": [vp, P(bt_camera), C.c_int, C.c_int, u32, u32],
     "bt_oracle_render": [vp, P(bt_camera), P(bt_render_config), C.c_int],
     "bt_render_frame": [vp, P(bt_camera), P(bt_render_config), u32, u32, C.c_int, C.c_int],
     "bt_gbuffer_download": [vp, vp, vp, vp, vp, vp, vp, vp],

@@ -109,6 +109,7 @@ struct GBuf {
     uint8_t* tileError = nullptr;
     uint32_t* fallback = nullptr;  // pixel indices needing the gradient normal
     int width = 0, height = 0, tilesX = 0, tilesY = 0;
+    int remote = 0;  // the planes are another GPU's (fused gather): fence the writes system-wide
 };
 
 inline Cam make_cam(const float* pos, const float* fwd, const float* right, const float* up,
@@ -183,10 +184,11 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
 // vb: the interval records of the march that produced this G-buffer (whole
 // frame, FMA path) -- the gradient fallback then evaluates the pruned view
 // of the interval each ray hit in; nullptr: the full tree (reference)
+// pixel rows [y0, y1) of the image (a sharded rank: its own tile rows)
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
-                    const ViewBufs* vb, bool zero = true);
+                    const ViewBufs* vb, bool zero = true, int y0 = 0, int y1 = -1);
 void launch_oracle(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                    const TraceParams& tp, const FrameBufs& fb, const GBuf& g, uint64_t* stats);
 

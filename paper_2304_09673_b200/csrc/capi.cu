@@ -150,7 +150,7 @@ struct bt_ctx {
     // planes straight into another context's G-buffer (CUDA IPC, peer memory)
     struct Remote {
         bool on = false;
-        void* p[6] = {};  // hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError
+        void* p[7] = {};  // hit, depth, evalCount, tileMaxOverlap, tileCacheBytes, tileError, normal
         int width = 0, height = 0;
     } remote;
 
@@ -299,6 +299,8 @@ GBuf trace_gbuf(const bt_ctx* c) {
         g.tileMaxOverlap = static_cast<uint32_t*>(c->remote.p[3]);
         g.tileCacheBytes = static_cast<uint32_t*>(c->remote.p[4]);
         g.tileError = static_cast<uint8_t*>(c->remote.p[5]);
+        g.normal = static_cast<float*>(c->remote.p[6]);
+        g.remote = 1;
     }
     return g;
 }
@@ -631,7 +633,9 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     return BT_OK;
 }
 
-int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
+// rows [y0, y1) of the image (y1 < 0: all); `target`: the planes to shade
+// (this context's, or the root's over peer memory for a sharded rank)
+int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact, int y0 = 0, int y1 = -1, bool target = false) {
     if (c->fullDepth > 128) return fail(BT_EINVAL, "full-tree evaluation stack deeper than 128 entries");
     if (c->gradWarps == 0) {
         // one CTA per queued pixel; frontier values live in shared memory,
@@ -648,9 +652,9 @@ int do_normals(bt_ctx* c, const bt_camera& cam, int mode, int exact) {
         c->bufEpoch++;
     }
     const ViewBufs vb = view_bufs(c);
-    launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), gbuf(c), mode,
-                   c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps,
-                   c->viewsFrame && !exact ? &vb : nullptr, !c->prezeroed);
+    launch_normals(c->stream, exact != 0, dev_tree(c), to_cam(cam), frame_bufs(c), target ? trace_gbuf(c) : gbuf(c),
+                   mode, c->counters.ptr, c->stats.ptr, c->smCount, c->gradScratch.ptr, c->gradWarps,
+                   (c->viewsFrame || target) && !exact ? &vb : nullptr, !c->prezeroed, y0, y1);
     return BT_OK;
 }
 
@@ -1242,6 +1246,29 @@ int bt_normals(bt_ctx* c, const bt_camera* cam, int mode, int exact) {
     return rc ? rc : launch_status();
 }
 
+int bt_normals_rows(bt_ctx* c, const bt_camera* cam, int mode, int exact, uint32_t tile0, uint32_t tile1) {
+    DevGuard dg_(c);
+    if (!c || !c->haveGbuffer) return fail(BT_ESTATE, "no G-buffer rendered");
+    int rc = check_camera(cam);
+    if (rc) return rc;
+    if (mode != 0 && mode != 1) return fail(BT_EINVAL, "unknown normals mode");
+    rc = resolve_tiles(c, tile0, tile1);
+    if (rc) return rc;
+    if (tile1 <= tile0) return BT_OK;
+    // the rows' pixels, plus one pixel row of halo on each side for the rays
+    const uint32_t tx = (uint32_t)c->tilesX, tiles = (uint32_t)(c->tilesX * c->tilesY);
+    const uint32_t r0 = tile0 / tx, r1 = (tile1 + tx - 1) / tx;
+    const uint32_t h0 = r0 > 0 ? (r0 - 1) * tx : 0u, h1 = std::min(tiles, (r1 + 1) * tx);
+    if (!rays_cover(c, *cam, h0, h1)) {
+        rc = do_camera(c, *cam, h0, h1);
+        if (rc) return rc;
+    }
+    prof_begin(c);
+    rc = do_normals(c, *cam, mode, exact, (int)(r0 * kTile), std::min((int)(r1 * kTile), c->height), true);
+    prof_end(c, 3);
+    return rc ? rc : launch_status();
+}
+
 int bt_oracle_render(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg, int exact) {
     DevGuard dg_(c);
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
@@ -1567,9 +1594,9 @@ int bt_gbuffer_export(bt_ctx* c, bt_ipc_handles* out) {
     DevGuard dg_(c);
     if (!c || !out) return fail(BT_EINVAL, "null argument");
     if (!c->hit.ptr) return fail(BT_ESTATE, "no G-buffer allocated (render a frame first)");
-    void* planes[6] = {c->hit.ptr, c->depth.ptr, c->evalCount.ptr, c->tileMaxOverlap.ptr, c->tileCacheBytes.ptr,
-                       c->tileError.ptr};
-    for (int i = 0; i < 6; ++i) {
+    void* planes[7] = {c->hit.ptr, c->depth.ptr, c->evalCount.ptr, c->tileMaxOverlap.ptr, c->tileCacheBytes.ptr,
+                       c->tileError.ptr, c->normal.ptr};
+    for (int i = 0; i < 7; ++i) {
         cudaIpcMemHandle_t h;
         BT_CUDA(cudaIpcGetMemHandle(&h, planes[i]));
         static_assert(sizeof(h) == sizeof(out->plane[0]), "IPC handle size");
@@ -1584,7 +1611,7 @@ int bt_gbuffer_import(bt_ctx* c, const bt_ipc_handles* in) {
     DevGuard dg_(c);
     if (!c || !in) return fail(BT_EINVAL, "null argument");
     release_remote(c);
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < 7; ++i) {
         cudaIpcMemHandle_t h;
         std::memcpy(&h, in->plane[i], sizeof(h));
         void* q = nullptr;

@@ -342,6 +342,10 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
         const uint32_t tile = vb.order ? vb.order[q] : tile0 + q;
         march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
+    // fused gather: this rank's pixels went to another GPU's planes; make
+    // them visible system-wide before the kernel ends (the completion
+    // collective that orders the root's normals follows on this stream)
+    if (g.remote) __threadfence_system();
     __syncthreads();
 #ifdef BT_STEP_HIST
     if (threadIdx.x == 0) {
@@ -413,10 +417,10 @@ __device__ __forceinline__ F3 position_at(const Cam& cam, const FrameBufs& fb, c
     return vadd<E>(cam.pos, vscale<E>(d, g.depth[(size_t)y * g.width + x]));
 }
 
-__global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* counters) {
+__global__ void k_normals(Cam cam, FrameBufs fb, GBuf g, int mode, uint32_t* counters, int y0, int y1) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= g.width || y >= g.height) return;
+    const int y = y0 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    if (x >= g.width || y >= y1) return;
     const size_t p = (size_t)y * g.width + x;
     float* nout = g.normal + 3 * p;
     if (!g.hit[p]) {
@@ -823,13 +827,16 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
                     const FrameBufs& fb, const GBuf& g, int mode, uint32_t* counters,
                     uint64_t* stats, int smCount, float* scratch, uint32_t scratchWarps,
-                    const ViewBufs* vb, bool zero) {
+                    const ViewBufs* vb, bool zero, int y0, int y1) {
     if (zero) {
         cudaMemsetAsync(counters + kCntFallback, 0, sizeof(uint32_t), st);
         cudaMemsetAsync(counters + kCntFallbackHard, 0, sizeof(uint32_t), st);
     }
-    dim3 block(16, 16), grid((g.width + 15) / 16, (g.height + 15) / 16);
-    k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters);
+    if (y1 < 0 || y1 > g.height) y1 = g.height;
+    if (y0 < 0) y0 = 0;
+    if (y1 <= y0) return;
+    dim3 block(16, 16), grid((g.width + 15) / 16, (y1 - y0 + 15) / 16);
+    k_normals<<<grid, block, 0, st>>>(cam, fb, g, mode, counters, y0, y1);
     const size_t bytes = (size_t)t.nFrontier * 6 * sizeof(float) + (size_t)t.nUpper * sizeof(uint32_t);
     const uint32_t useSmem = bytes <= kGradSmemBytes ? 1u : 0u;
     const size_t smem = useSmem ? bytes : 0;

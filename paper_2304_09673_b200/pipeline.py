@@ -286,6 +286,11 @@ class Renderer:
     def compute_normals(self, cam: bt_camera, mode: int = 0, exact: bool = True) -> None:
         check(self.lib.bt_normals(self.ctx, C.byref(cam), mode, int(exact)), "bt_normals")
 
+    def compute_normals_rows(self, cam: bt_camera, tile0: int, tile1: int, mode: int = 0, exact: bool = True) -> None:
+        """Normals of the tile rows covering [tile0, tile1) only (a sharded
+        rank; into the root's planes when a G-buffer is imported)."""
+        check(self.lib.bt_normals_rows(self.ctx, C.byref(cam), mode, int(exact), tile0, tile1), "bt_normals_rows")
+
     def oracle_render(self, cam: bt_camera, cfg: RenderConfig, exact: bool = True) -> None:
         c = cfg.to_c()
         check(self.lib.bt_oracle_render(self.ctx, C.byref(cam), C.byref(c), int(exact)), "bt_oracle_render")
