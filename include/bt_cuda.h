@@ -269,6 +269,16 @@ BT_API int bt_gbuffer_import_release(bt_ctx* ctx);
  * bt_set_tile_order installs a fixed host-given permutation of all tiles
  * instead (mode 2, full frames).  Results never depend on the order. */
 BT_API int bt_set_scheduling(bt_ctx* ctx, int mode);
+/* Step bound of the sphere trace (tracer.hpp:99-177).  Mode 0 (default):
+ * the reference's global Lipschitz bound cfg.lipschitz for every interval.
+ * Mode 1 (extension, PAPER.md "Ray processing": "replacing sphere-tracing
+ * with segment-tracing would provide a more robust solution"): a bound per
+ * interval view -- a view made only of exact distances (sphere, torus, box,
+ * sphere-cone) and sharp CSG is 1-Lipschitz and marches with L = 1; every
+ * other view keeps cfg.lipschitz.  The trajectory changes, so mode 1 is
+ * held to its own tolerance contract against the reference
+ * (tests/test_gpu_step_bound.py), never to bit-exactness. */
+BT_API int bt_set_step_bound(bt_ctx* ctx, int mode);
 BT_API int bt_set_tile_order(bt_ctx* ctx, const uint32_t* order, uint32_t n);
 BT_API int bt_gbuffer_device(bt_ctx* ctx, bt_gbuffer_view* out);
 /* hit/depth planes from the host (compute_normals on a caller's G-buffer) */

@@ -300,6 +300,25 @@ BT_DEV float eval_comb(const uint2* rec, uint32_t nPrims, const float4* blk, F3 
     return v;
 }
 
+// eval_comb plus the CSG margin of its compact operators: min over them of
+// max(f0, f1) - d (> 0: every one is in its CSG branch, field.cpp:431)
+BT_DEV float eval_comb_margin(const uint2* rec, uint32_t nPrims, const float4* blk, F3 p, float& margin) {
+    uint32_t rx = rec[0].x;
+    float v = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
+    float mg = f_inf();
+    for (uint32_t j = 1; j < nPrims; ++j) {
+        const uint2 r = rec[j];
+        rx = r.x;
+        const uint32_t ry = r.y, code = ry & 15u;
+        const float4* Bo = blk + (ry >> 4);
+        const float w = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
+        if (code >= 9u) mg = fminf(mg, fmaxf(v, w) - Bo[0].y);
+        v = comb_op(code, Bo, v, w);
+    }
+    margin = mg;
+    return v;
+}
+
 constexpr uint32_t kNotAnOp = 0x80000000u;  // a primitive header: ends a fused primitive + operator pair
 
 // Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks in

@@ -42,7 +42,27 @@ struct TraceParams {
     float L, invL, relax, minStep, hitEps;
     uint32_t maxOverlap, maxNew;
     float window;  // resolved fetch window in view-z units
+    uint32_t viewLipschitz;  // step bound per view (bt_set_step_bound): 1-Lipschitz views march with L = 1
 };
+
+// A view whose field is 1-Lipschitz: exact signed distances (sphere, torus,
+// box, sphere-cone: field.cpp:219-254 are the Euclidean distances) combined
+// only by sharp CSG (min / max / max(a, -b)) and the reserved pass-through
+// codes, all of which preserve the Lipschitz constant 1.  The ellipsoid and
+// quadric are first-order approximations and the smooth / compact blends
+// compress the field (the reason for the global bound L = 1.45, PAPER.md
+// "Ray processing"), so any of them keeps the configured bound.
+BT_HD bool node_is_one_lipschitz(uint32_t hdr) {
+    const uint32_t op = blob_op(hdr);
+    if (blob_is_prim(hdr)) return op == 0u || op == 2u || op == 3u || op == 4u;
+    return op <= 5u;
+}
+// ... or becomes 1-Lipschitz where every compact operator (codes 9-11) is in
+// its CSG branch: max(f0, f1) > d (field.cpp:424-440) -- the compact blends
+// are exactly CSG outside their support, which is their point
+BT_HD bool node_is_lipschitz_capable(uint32_t hdr) {
+    return node_is_one_lipschitz(hdr) || (!blob_is_prim(hdr) && blob_op(hdr) >= 9u && blob_op(hdr) <= 11u);
+}
 
 struct Frag {
     uint32_t word;
@@ -110,6 +130,10 @@ BT_DEV float eval_staged(const uint32_t* hdr, const uint32_t* word, uint32_t n, 
 //   kHitFlag on completion: t holds the hit position.
 constexpr uint32_t kPhaseMask = 3u;
 constexpr uint32_t kSaved = 4u, kHitFlag = 8u;
+// bt_set_step_bound(1), comb views with compact operators: the step from the
+// accepted point t (kLipT) / from the saved sphere (kLipS) was bounded with
+// L = 1 (see march_consume)
+constexpr uint32_t kLipT = 16u, kLipS = 32u;
 
 struct March {
     float t, f, t1, savedT, savedF, evalT;
@@ -151,7 +175,16 @@ BT_DEV void march_begin(March& m, float t0, float t1) {
 // unconditionally and committed by predicates: a warp whose lanes hit,
 // miss, overshoot, back off or re-use a sphere in the same step never
 // diverges.
-BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
+// Lip = true (bt_set_step_bound(1) on a comb view with compact operators):
+// the bound L of each step is chosen at the sample the step starts from --
+// 1 when `lip1` (every compact operator of the view is in its CSG branch
+// with a margin max(f0, f1) - d above the relaxed step length, and every
+// primitive is an exact distance, so the field is 1-Lipschitz over the whole
+// step: each operand moves by at most the step length), else tp.L -- and
+// remembered for the overshoot test, the back-off and the saved sphere.
+// Lip = false is the reference's loop with the global bound.
+template <bool Lip = false>
+BT_DEV void march_consume(March& m, float v, const TraceParams& tp, bool lip1 = false) {
     // Boolean algebra with & | (no short-circuit branches) and FMNMX for the
     // step maxima: max(x, minStep) with minStep > 0 equals std::max except
     // for a NaN x, and a NaN x only arises from a non-finite f/L, which ends
@@ -161,19 +194,21 @@ BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     const bool mainStep = (m.st & 2u) != 0u;
     const bool sv = (m.st & kSaved) != 0u;
     const float sT = m.savedT, sF = m.savedF;
+    const float Lt = Lip && (m.st & kLipT) ? 1.0f : tp.L, invLt = Lip && (m.st & kLipT) ? 1.0f : tp.invL;
+    const float invLn = Lip && lip1 ? 1.0f : tp.invL, invLs = Lip && (m.st & kLipS) ? 1.0f : tp.invL;
     const bool ovT = mainStep & !sv &
-                     ((E::mul(E::sub(tn, m.t), tp.L) >= E::add(m.f, fabsf(v))) | (v < -tp.hitEps));
-    const float tb = E::add(m.t, fmaxf(E::mul(m.f, tp.invL), tp.minStep));
+                     ((E::mul(E::sub(tn, m.t), Lt) >= E::add(m.f, fabsf(v))) | (v < -tp.hitEps));
+    const float tb = E::add(m.t, fmaxf(E::mul(m.f, invLt), tp.minStep));
     const bool ov = ovT & !(tb >= tn);
     const bool hit1 = !ov & (v <= tp.hitEps);
     // advance from the accepted (tn, v)
-    const float r = E::mul(v, tp.invL);
+    const float r = E::mul(v, invLn);
     const bool fin = is_finite(r);
     const float tnA = E::add(tn, fmaxf(sv ? r : E::mul(tp.relax, r), tp.minStep));
     const bool reach = sv & !hit1 & fin & (tnA >= sT);  // sv implies !ov
     const bool reuse = reach & (sT >= E::add(tn, tp.minStep)) & (sT <= m.t1);
     // ... re-using the saved sphere, then one relaxed advance from it
-    const float r2 = E::mul(sF, tp.invL);
+    const float r2 = E::mul(sF, invLs);
     const float tn2 = E::add(sT, fmaxf(E::mul(tp.relax, r2), tp.minStep));
     const bool hit2 = reuse & (sF <= tp.hitEps);
     const float T = reuse ? sT : tn;  // the accepted point the next step starts from
@@ -187,7 +222,12 @@ BT_DEV void march_consume(March& m, float v, const TraceParams& tp) {
     m.t = ov ? m.t : T;
     m.f = ov ? m.f : (reuse ? sF : v);
     m.evalT = ov ? tb : (beyond ? m.t1 : En);
-    const uint32_t next = ((ov | (sv & !reach)) ? kSaved : 0u) | (ov ? 1u : 2u);
+    uint32_t next = ((ov | (sv & !reach)) ? kSaved : 0u) | (ov ? 1u : 2u);
+    if (Lip) {
+        const uint32_t lipT = ov ? (m.st & kLipT) : ((reuse ? (m.st & kLipS) != 0u : lip1) ? kLipT : 0u);
+        const uint32_t lipS = ov ? (lip1 ? kLipS : 0u) : ((sv & !reach) ? (m.st & kLipS) : 0u);
+        next |= lipT | lipS;
+    }
     m.st = hit ? kHitFlag : (miss ? 0u : next);
 }
 

@@ -163,6 +163,7 @@ struct bt_ctx {
     DevBuf<uint32_t> tileOrder, tileCost, orderHist, hostUnits;
     bool viewsFrame = false;  // the G-buffer came from a whole-frame FMA-path march (its records are valid)
     int schedMode = 1;
+    int stepBound = 0;  // 0 reference (global L), 1 view-local Lipschitz bound (bt_set_step_bound)
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
@@ -409,8 +410,9 @@ void prof_end(bt_ctx* c, int slot) {
     c->profLaunch[slot] += 1;
 }
 
-TraceParams trace_params(const bt_render_config& cfg, const bt_camera& cam) {
+TraceParams trace_params(const bt_render_config& cfg, const bt_camera& cam, int stepBound = 0) {
     TraceParams tp;
+    tp.viewLipschitz = stepBound == 1 ? 1u : 0u;
     tp.L = cfg.lipschitz;
     tp.invL = 1.0f / cfg.lipschitz;
     tp.relax = cfg.relax;
@@ -576,7 +578,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     const DevTree t = dev_tree(c);
     const Cam k = to_cam(cam);
-    const TraceParams tp = trace_params(cfg, cam);
+    const TraceParams tp = trace_params(cfg, cam, c->stepBound);
     // stage events only in eager frames: synchronising on an event inside a
     // stream capture would invalidate the capture
     const bool prof = c->profiling && checked;
@@ -1338,7 +1340,7 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         else BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[0], 0));
         if (r) return r;
         // one per-tile pass builds each tile's fragment list AND its interval records
-        const TraceParams tp = trace_params(*cfg, *cam);
+        const TraceParams tp = trace_params(*cfg, *cam, c->stepBound);
         r = do_abuffer(c, *cam, tile0, tile1, checked, kTileRaster | kTileViews, &tp);
         if (r) return r;
         r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked, true);
@@ -1578,6 +1580,17 @@ int bt_set_tile_order(bt_ctx* c, const uint32_t* order, uint32_t n) {
     BT_CUDA(cudaStreamSynchronize(c->stream));
     c->schedMode = 2;
     c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_set_step_bound(bt_ctx* c, int mode) {
+    DevGuard dg_(c);
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (mode != 0 && mode != 1) return fail(BT_EINVAL, "step bound mode must be 0 or 1");
+    if (mode != c->stepBound) {
+        c->stepBound = mode;
+        c->bufEpoch++;  // re-capture the frame graph
+    }
     return BT_OK;
 }
 

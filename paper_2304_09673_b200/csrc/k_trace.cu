@@ -98,6 +98,7 @@ constexpr int kClsRaw = 0;      // raw tree parameters (exact path, or a view to
 constexpr int kClsGeneral = 1;  // fast blocks, interpreter
 constexpr int kClsSingle = 2;   // fast blocks, one primitive
 constexpr int kClsComb = 3;     // fast blocks, left comb P (P O)*
+constexpr int kClsCombLip = 4;  // ... with a step bound per sample (bt_set_step_bound(1), compact operators)
 
 // March the pending rays of one interval over the staged view.  `aux`:
 // single -> the primitive's comb record; comb -> the primitive count.
@@ -154,11 +155,18 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
 #endif
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
+        float margin = 0.0f;
         if constexpr (Cls == kClsSingle) v = fast_prim(comb_rec_kind(uaux), s.blocks + (uaux >> 5), p);
         else if constexpr (Cls == kClsComb) v = eval_comb(s.rec, uaux, s.blocks, p);
+        else if constexpr (Cls == kClsCombLip) v = eval_comb_margin(s.rec, uaux, s.blocks, p, margin);
         else if constexpr (Cls == kClsGeneral) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
         else v = eval_staged<O>(s.hdr, s.word, nView, t.words, p);  // exact path, or an oversized view
-        if (march_phase(m) != 0u) march_consume(m, v, tp);
+        if constexpr (Cls == kClsCombLip) {
+            const bool lip1 = margin > fmaxf(tp.relax * v, tp.minStep);
+            if (march_phase(m) != 0u) march_consume<true>(m, v, tp, lip1);
+        } else {
+            if (march_phase(m) != 0u) march_consume(m, v, tp);
+        }
     }
 }
 
@@ -229,10 +237,12 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             // fast path: evaluation-ready parameter blocks in shared memory when
             // the view fits (the common case); otherwise raw parameters
             const bool fits = IsFast<O>::value && rb.w <= kMarchBlocks;
-            bool notComb = false;
+            bool notComb = false, notLip1 = false, notLipCap = false;
             for (uint32_t i = lane; i < nView; i += 32) {
                 const uint2 nd = vb.nodes[ra.z + i];
                 s.hdr[i] = nd.x;
+                notLip1 |= !node_is_one_lipschitz(nd.x);
+                notLipCap |= !node_is_lipschitz_capable(nd.x);
                 if (fits) {
                     convert_node(nd.x, t.words + nd.y + 1, s.blocks + ((nd.x & 0xFFFFu) >> 4));
                     // left comb: node 0 and every odd node a primitive, every even node > 0 an operator
@@ -245,6 +255,18 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
                 }
             }
             const bool comb = fits && !__any_sync(kFull, notComb) && (nView & 1u);
+            // step bound of this interval: the configured L, or 1 for a
+            // 1-Lipschitz view when the view-local bound is enabled
+            TraceParams tpi = tp;
+            bool combLip = false;  // a comb whose compact operators may leave it 1-Lipschitz, step by step
+            if (tp.viewLipschitz) {
+                if (!__any_sync(kFull, notLip1)) {
+                    tpi.L = 1.0f;
+                    tpi.invL = 1.0f;
+                } else {
+                    combLip = comb && !__any_sync(kFull, notLipCap);
+                }
+            }
             // queue of this interval: the tile's unfinished rays, in ray order
             const uint32_t p0 = ~found0, p1 = ~found1;
             const uint32_t c0 = __popc(p0), nPend = c0 + __popc(p1);
@@ -255,18 +277,21 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             uint32_t ife = 0, ifl = 0, isteps = 0;
             if constexpr (IsFast<O>::value) {
                 if (nView == 1u && comb)
-                    march_interval<O, kClsSingle>(t, cam, tp, s, s.rec[0].x, nView, nPend, vz0, vz1, lt, ife, ifl,
+                    march_interval<O, kClsSingle>(t, cam, tpi, s, s.rec[0].x, nView, nPend, vz0, vz1, lt, ife, ifl,
                                                   isteps, rb.z);
+                else if (combLip)
+                    march_interval<O, kClsCombLip>(t, cam, tpi, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt,
+                                                   ife, ifl, isteps, rb.z);
                 else if (comb)
-                    march_interval<O, kClsComb>(t, cam, tp, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt, ife,
+                    march_interval<O, kClsComb>(t, cam, tpi, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt, ife,
                                                 ifl, isteps, rb.z);
                 else if (fits)
-                    march_interval<O, kClsGeneral>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps,
+                    march_interval<O, kClsGeneral>(t, cam, tpi, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps,
                                                    rb.z);
                 else
-                    march_interval<O, kClsRaw>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+                    march_interval<O, kClsRaw>(t, cam, tpi, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
             } else {
-                march_interval<O, kClsRaw>(t, cam, tp, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
+                march_interval<O, kClsRaw>(t, cam, tpi, s, 0u, nView, nPend, vz0, vz1, lt, ife, ifl, isteps, rb.z);
             }
             s.accFe[lane] += ife;
             s.accFl[lane] += ifl;

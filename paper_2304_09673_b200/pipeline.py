@@ -286,6 +286,11 @@ class Renderer:
     def compute_normals(self, cam: bt_camera, mode: int = 0, exact: bool = True) -> None:
         check(self.lib.bt_normals(self.ctx, C.byref(cam), mode, int(exact)), "bt_normals")
 
+    def set_step_bound(self, mode: int) -> None:
+        """0: the reference's global Lipschitz bound; 1: a bound per interval
+        view (1-Lipschitz views march with L = 1; bt_set_step_bound)."""
+        check(self.lib.bt_set_step_bound(self.ctx, int(mode)), "bt_set_step_bound")
+
     def compute_normals_rows(self, cam: bt_camera, tile0: int, tile1: int, mode: int = 0, exact: bool = True) -> None:
         """Normals of the tile rows covering [tile0, tile1) only (a sharded
         rank; into the root's planes when a G-buffer is imported)."""
