@@ -131,7 +131,10 @@ def load() -> C.CDLL:
         raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()) first; "
                           "there is no CPU fallback for the blobtree-b200 hot path")
     lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    lenient = os.environ.get("BT_CAPI_LENIENT") == "1"  # A/B timing against older builds (scripts/ab_multi.sh)
     for name, args in PROTOTYPES.items():
+        if lenient and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int

@@ -183,7 +183,7 @@ __device__ __forceinline__ void unit_rays(const GBuf& g, int tx, int ty, uint32_
 // (tracer.cpp:165-230), then write its pixels and tile planes.  The tile's
 // bookkeeping lives in the warp's shared memory, not in registers that would
 // stay live across the march loop.
-template <class O>
+template <class O, bool SB = false>
 __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
                                            const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
                                            BlockStats& bs, int lane, uint32_t unit) {
@@ -241,8 +241,10 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             for (uint32_t i = lane; i < nView; i += 32) {
                 const uint2 nd = vb.nodes[ra.z + i];
                 s.hdr[i] = nd.x;
-                notLip1 |= !node_is_one_lipschitz(nd.x);
-                notLipCap |= !node_is_lipschitz_capable(nd.x);
+                if (SB) {
+                    notLip1 |= !node_is_one_lipschitz(nd.x);
+                    notLipCap |= !node_is_lipschitz_capable(nd.x);
+                }
                 if (fits) {
                     convert_node(nd.x, t.words + nd.y + 1, s.blocks + ((nd.x & 0xFFFFu) >> 4));
                     // left comb: node 0 and every odd node a primitive, every even node > 0 an operator
@@ -259,7 +261,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             // 1-Lipschitz view when the view-local bound is enabled
             TraceParams tpi = tp;
             bool combLip = false;  // a comb whose compact operators may leave it 1-Lipschitz, step by step
-            if (tp.viewLipschitz) {
+            if (SB && tp.viewLipschitz) {
                 if (!__any_sync(kFull, notLip1)) {
                     tpi.L = 1.0f;
                     tpi.invL = 1.0f;
@@ -279,9 +281,9 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
                 if (nView == 1u && comb)
                     march_interval<O, kClsSingle>(t, cam, tpi, s, s.rec[0].x, nView, nPend, vz0, vz1, lt, ife, ifl,
                                                   isteps, rb.z);
-                else if (combLip)
-                    march_interval<O, kClsCombLip>(t, cam, tpi, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt,
-                                                   ife, ifl, isteps, rb.z);
+                else if (SB && combLip)  // (the step-bound kernel only: keeps the default kernel's code small)
+                    march_interval<O, SB ? kClsCombLip : kClsComb>(t, cam, tpi, s, (nView + 1u) >> 1, nView, nPend,
+                                                                   vz0, vz1, lt, ife, ifl, isteps, rb.z);
                 else if (comb)
                     march_interval<O, kClsComb>(t, cam, tpi, s, (nView + 1u) >> 1, nView, nPend, vz0, vz1, lt, ife,
                                                 ifl, isteps, rb.z);
@@ -347,7 +349,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
 
 // Persistent kernel: each warp pulls tiles from a queue (tiles differ wildly
 // in cost -- empty tiles exit at once).
-template <class O, int MinBlocks>
+template <class O, int MinBlocks, bool SB = false>
 __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     k_march(DevTree t, Cam cam, TraceParams tp, FrameBufs fb, ViewBufs vb, GBuf g, uint64_t* stats, uint32_t tile0,
             uint32_t tile1, uint32_t* tileQueue) {
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
         q = __shfl_sync(kFull, q, 0);
         if (q >= nUnits) break;
         const uint32_t tile = vb.order ? vb.order[q] : tile0 + q;
-        march_tile<O>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
+        march_tile<O, SB>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
     }
     // fused gather: this rank's pixels went to another GPU's planes; make
     // them visible system-wide before the kernel ends (the completion
@@ -797,7 +799,10 @@ int trace_min_blocks() {
     return mb;
 }
 
-void* trace_fn(bool exact) {
+void* trace_fn(bool exact, bool stepBound = false) {
+    // the view-local step bound (bt_set_step_bound(1), FMA path) is its own
+    // kernel, at the default register budget
+    if (stepBound && !exact) return (void*)k_march<FastOps, kDefaultMinBlocks, true>;
     switch (trace_min_blocks()) {
         case 4: return TraceVariant<4>::fn(exact);
         case 5: return TraceVariant<5>::fn(exact);
@@ -822,12 +827,12 @@ uint32_t trace_grid_blocks(int smCount) {
     if (perSM == 0) {
         const size_t smem = sizeof(MarchSmem) * kTraceWarps;
         int best = 1;
-        for (int ex = 0; ex < 2; ++ex) {
-            const void* f = trace_fn(ex != 0);
+        for (int v = 0; v < 3; ++v) {
+            const void* f = trace_fn(v == 1, v == 2);
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int a = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, f, kTraceWarps * 32, smem);
-            best = std::max(best, a);
+            if (v < 2) best = std::max(best, a);
         }
         perSM = best;
     }
@@ -846,7 +851,7 @@ void launch_trace(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
     if (zero) cudaMemsetAsync(tileQueue, 0, sizeof(uint32_t), st);
     void* args[] = {(void*)&t,    (void*)&cam,   (void*)&tp,    (void*)&fb,          (void*)&vb,       (void*)&g,
                     (void*)&stats, (void*)&tile0, (void*)&tile1, (void*)&tileQueue};
-    cudaLaunchKernel(trace_fn(exact), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
+    cudaLaunchKernel(trace_fn(exact, tp.viewLipschitz != 0), dim3(blocks), dim3(kTraceWarps * 32), args, smem, st);
 }
 
 void launch_normals(cudaStream_t st, bool exact, const DevTree& t, const Cam& cam,
