@@ -40,11 +40,21 @@ constexpr uint32_t kTileStage = 256;  // fragments of a tile sorted in shared me
 // and kSlabWords active words in total (more: the fetch is replayed)
 constexpr uint32_t kSlabIv = 32, kSlabWords = 192;
 
+constexpr uint32_t kSmallIv = 136;  // intervals of a <= 32-fragment tile kept: at most 4 F + 2 (k_tile_views)
+
 struct TileSmem {  // views pass, per warp
-    WarpFetchSmem wf;
-    float ivZb[kSlabIv], ivZe[kSlabIv];
-    uint32_t ivN[kSlabIv];
-    uint32_t words[kSlabWords];
+    union {
+        struct {  // WarpFetch path (tiles of more than 32 fragments)
+            WarpFetchSmem wf;
+            float ivZb[kSlabIv], ivZe[kSlabIv];
+            uint32_t ivN[kSlabIv];
+            uint32_t words[kSlabWords];
+        } big;
+        struct {  // lane-per-fragment path: an interval's active set is a lane mask
+            float zb[kSmallIv], ze[kSmallIv];
+            uint32_t act[kSmallIv];
+        } small;
+    };
 };
 
 // The exact interval of one volume over the tile's rays (abuffer.cpp:198-216):
@@ -174,6 +184,17 @@ __device__ __forceinline__ void sort_tile(const uint4* src, uint32_t n, Frag* ds
     }
 }
 
+// The march cost proxy of a tile (longest-first scheduling): 2 x fragments +
+// the view-node bound (2 nAct - 1 per interval) weighted by the interval's
+// view-z length in fetch windows (1x .. 4x) + 16 x the summed NDC depth
+// extent of the fragments (variants compared with scripts/proxy_ab.sh)
+__device__ __forceinline__ float interval_cost(const Cam& cam, const TraceParams& tp, float zb, float ze, uint32_t n) {
+    const float dvz = FastOps::rcp(cam.invNear - ze * FastOps::rcp(cam.invDepthRange)) -
+                      FastOps::rcp(cam.invNear - zb * FastOps::rcp(cam.invDepthRange));
+    const float rel = fmaxf(dvz, 0.0f) * FastOps::rcp(tp.window);
+    return (float)(2u * n - 1u) * fminf(4.0f, 1.0f + 4.0f * rel);
+}
+
 // The tile's interval sequence (WarpFetch over its sorted list) -> interval
 // records + active words, bump-allocated; vb.count / vb.base / tileCost.
 __device__ void views_tile(const Cam& cam, const TraceParams& tp, const FrameBufs& fb, const ViewBufs& vb,
@@ -186,30 +207,25 @@ __device__ void views_tile(const Cam& cam, const TraceParams& tp, const FrameBuf
     const Frag* list = fb.frags + fbase;
     if (cnt) {
         WarpFetch f;
-        f.init(list, cnt, &S.wf, lane);
+        f.init(list, cnt, &S.big.wf, lane);
         float zb;
         while (f.next<true>(cam, tp, zb)) {
             const uint32_t n = f.n;
             if (kept && (c.x >= kSlabIv || words + n > kSlabWords)) kept = false;
             if (kept) {
                 if (lane == 0) {
-                    S.ivZb[c.x] = zb;
-                    S.ivZe[c.x] = f.zEnd;
-                    S.ivN[c.x] = n;
+                    S.big.ivZb[c.x] = zb;
+                    S.big.ivZe[c.x] = f.zEnd;
+                    S.big.ivN[c.x] = n;
                 }
 #pragma unroll
                 for (int sl = 0; sl < 3; ++sl)
-                    if (lane + 32u * sl < n) S.words[words + lane + 32u * sl] = f.aW[sl];
+                    if (lane + 32u * sl < n) S.big.words[words + lane + 32u * sl] = f.aW[sl];
                 words += n;
             }
             c.x += 1u;
             c.y += 2u * n - 1u;
-            {  // view-node bound weighted by the interval's length in view z (fetch windows)
-                const float dvz = FastOps::rcp(cam.invNear - f.zEnd * FastOps::rcp(cam.invDepthRange)) -
-                                  FastOps::rcp(cam.invNear - zb * FastOps::rcp(cam.invDepthRange));
-                const float rel = fmaxf(dvz, 0.0f) * FastOps::rcp(tp.window);
-                wsum += (float)(2u * n - 1u) * fminf(4.0f, 1.0f + 4.0f * rel);
-            }
+            wsum += interval_cost(cam, tp, zb, f.zEnd, n);
         }
     }
     // march cost proxy for longest-first scheduling: 2 x fragments + the
@@ -242,13 +258,13 @@ __device__ void views_tile(const Cam& cam, const TraceParams& tp, const FrameBuf
         __syncwarp();
         uint32_t w = 0;
         for (uint32_t k = 0; k < c.x; ++k) {
-            const uint32_t n = S.ivN[k];
+            const uint32_t n = S.big.ivN[k];
             uint2* act = vb.nodes + nodeOff + n - 1u;
-            for (uint32_t j = lane; j < n; j += 32) act[j].x = S.words[w + j];
+            for (uint32_t j = lane; j < n; j += 32) act[j].x = S.big.words[w + j];
             if (lane == 0) {
                 IntervalRec& r = vb.iv[base.x + k];
-                r.zBegin = S.ivZb[k];
-                r.zEnd = S.ivZe[k];
+                r.zBegin = S.big.ivZb[k];
+                r.zEnd = S.big.ivZe[k];
                 r.nodeOff = nodeOff;
                 r.actFlags = n;
             }
@@ -258,7 +274,7 @@ __device__ void views_tile(const Cam& cam, const TraceParams& tp, const FrameBuf
         return;
     }
     WarpFetch f;  // too many intervals for the slab: replay the fetch sequence
-    f.init(list, cnt, &S.wf, lane);
+    f.init(list, cnt, &S.big.wf, lane);
     float zb;
     for (uint32_t k = 0; k < c.x && f.next<true>(cam, tp, zb); ++k) {
         const uint32_t n = f.n;
@@ -275,6 +291,162 @@ __device__ void views_tile(const Cam& cam, const TraceParams& tp, const FrameBuf
         }
         nodeOff += 2u * n - 1u;
     }
+}
+
+// fetch_interval (tracer.cpp:50-103) for a tile of at most 32 fragments,
+// lane j holding fragment j of the sorted list: the active set is a lane
+// mask, expiry one ballot, the fetch one segmented prefix-max scan of the
+// exits, and the word order of the actives a popcount against each lane's
+// static "words below mine" mask.  The view z of every entry (the window
+// test) is computed once per fragment.  Same compares and exact operations
+// as WarpFetch (bt_views.cuh) -- bit-identical intervals and active sets.
+struct LaneFetch {
+    uint32_t w;
+    float en, ex, vzEn;
+    uint32_t cnt, lane, active, n, cursor;
+    float zEnd;
+
+    BT_DEV void init(const Frag* list, uint32_t count, const Cam& cam) {
+        lane = threadIdx.x & 31u;
+        cnt = count;
+        w = 0xFFFFFFFFu;
+        en = f_inf();
+        ex = -f_inf();
+        vzEn = 0.0f;
+        if (lane < count) {
+            const Frag f = list[lane];
+            w = f.word;
+            en = f.zEntry;
+            ex = f.zExit;
+            vzEn = view_z_from_ndc(cam, en);
+        }
+        active = 0u;
+        n = 0u;
+        cursor = 0u;
+        zEnd = 0.0f;
+    }
+
+    BT_DEV bool next(const Cam& cam, const TraceParams& tp, float& zBeginOut) {
+        constexpr uint32_t kF = 0xFFFFFFFFu;
+        const float zEndPrev = zEnd;
+        const bool mine = (active >> lane) & 1u;
+        const uint32_t expMask = __ballot_sync(kF, mine && ex <= zEndPrev);
+        const bool expired = expMask != 0u;
+        active &= ~expMask;
+        n = __popc(active);
+        const bool hasNext = cursor < cnt;
+        if (n == 0u && !hasNext) return false;
+        float zBegin = zEndPrev;
+        if (hasNext) zBegin = smax(zEndPrev, __shfl_sync(kF, en, cursor));
+        const float zBeginView = view_z_from_ndc(cam, zBegin);
+        float maxExit = ((active >> lane) & 1u) ? ex : -f_inf();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxExit = fmaxf(maxExit, __shfl_xor_sync(kF, maxExit, o));
+        // candidates cursor .. cnt-1: inclusive prefix max of their exits
+        const bool cand = lane >= cursor && lane < cnt;
+        float inclMax = cand ? ex : -f_inf();
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float v = __shfl_up_sync(kF, inclMax, o);
+            if (lane >= (uint32_t)o) inclMax = fmaxf(inclMax, v);
+        }
+        float exclMax = __shfl_up_sync(kF, inclMax, 1);
+        if (lane == 0) exclMax = -f_inf();
+        bool ok = false;
+        if (cand) {
+            const uint32_t fj = lane - cursor, nj = n + fj;
+            const float mx = fmaxf(maxExit, exclMax);
+            ok = nj == 0u || !(en > mx || fj >= tp.maxNew || nj >= tp.maxOverlap ||
+                               E::sub(vzEn, zBeginView) >= tp.window);
+        }
+        const uint32_t okMask = __ballot_sync(kF, ok) >> cursor;  // candidates in list order
+        const uint32_t fetched = okMask == 0xFFFFFFFFu ? 32u : (uint32_t)(__ffs(~okMask) - 1);
+        if (fetched) {
+            maxExit = fmaxf(maxExit, __shfl_sync(kF, inclMax, cursor + fetched - 1u));
+            active |= (fetched >= 32u ? 0xFFFFFFFFu : ((1u << fetched) - 1u)) << cursor;
+            n += fetched;
+            cursor += fetched;
+        }
+        float zEndNew = maxExit;
+        if (cursor < cnt) zEndNew = smin(__shfl_sync(kF, en, cursor), maxExit);
+        if (zEndNew <= zBegin && fetched == 0u && !expired) {
+            float minExit = ((active >> lane) & 1u) ? ex : f_inf();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) minExit = fminf(minExit, __shfl_xor_sync(kF, minExit, o));
+            zEndNew = minExit;
+        }
+        zEnd = zEndNew;
+        zBeginOut = zBegin;
+        return true;
+    }
+};
+
+// views_tile for a tile of at most 32 fragments (LaneFetch)
+__device__ void views_tile_small(const Cam& cam, const TraceParams& tp, const FrameBufs& fb, const ViewBufs& vb,
+                                 TileSmem& S, uint32_t tile, uint32_t fbase, uint32_t cnt) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const Frag* list = fb.frags + fbase;
+    LaneFetch f;
+    f.init(list, cnt, cam);
+    // static word order: the lanes whose word is below mine (words are unique in a tile)
+    uint32_t below = 0u;
+    for (uint32_t k = 0; k < cnt; ++k) below |= (__shfl_sync(kFull, f.w, k) < f.w ? 1u : 0u) << k;
+    uint2 c = make_uint2(0u, 0u);
+    float wsum = 0.0f;
+    bool kept = true;
+    float zb;
+    while (f.next(cam, tp, zb)) {
+        if (c.x >= kSmallIv) kept = false;
+        if (kept && lane == 0) {
+            S.small.zb[c.x] = zb;
+            S.small.ze[c.x] = f.zEnd;
+            S.small.act[c.x] = f.active;
+        }
+        c.x += 1u;
+        c.y += 2u * f.n - 1u;
+        wsum += interval_cost(cam, tp, zb, f.zEnd, f.n);
+    }
+    float span = lane < cnt ? f.ex - f.en : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(kFull, span, o);
+    uint2 base = make_uint2(0u, 0u);
+    if (lane == 0) {
+        vb.tileCost[tile] = min(255u, 2u * cnt + (uint32_t)wsum + (uint32_t)(16.0f * fmaxf(span, 0.0f)));
+        if (c.x) {
+            base.x = atomicAdd(&vb.counters[2], c.x);
+            base.y = atomicAdd(&vb.counters[3], c.y);
+        }
+    }
+    base.x = __shfl_sync(kFull, base.x, 0);
+    base.y = __shfl_sync(kFull, base.y, 0);
+    const bool fits = (uint64_t)base.x + c.x <= vb.ivCap && (uint64_t)base.y + c.y <= vb.nodeCap;
+    if (lane == 0) {
+        vb.count[tile] = c;
+        vb.base[tile] = base;
+        if (c.x && !fits) atomicExch(&vb.counters[1], 1u);  // the march flags the frame's tiles
+    }
+    if (!c.x || !fits) return;
+    uint32_t nodeOff = base.y;
+    auto emit = [&](uint32_t k, float zBegin, float zEnd, uint32_t act) {
+        const uint32_t n = __popc(act);
+        // active words in word order into the last n of the 2n - 1 node slots
+        if ((act >> lane) & 1u) vb.nodes[nodeOff + n - 1u + __popc(act & below)].x = f.w;
+        if (lane == 0) {
+            IntervalRec& r = vb.iv[base.x + k];
+            r.zBegin = zBegin;
+            r.zEnd = zEnd;
+            r.nodeOff = nodeOff;
+            r.actFlags = n;
+        }
+        nodeOff += 2u * n - 1u;
+    };
+    if (kept) {
+        __syncwarp();
+        for (uint32_t k = 0; k < c.x; ++k) emit(k, S.small.zb[k], S.small.ze[k], S.small.act[k]);
+        return;
+    }
+    f.init(list, cnt, cam);  // more intervals than kept: replay
+    for (uint32_t k = 0; k < c.x && f.next(cam, tp, zb); ++k) emit(k, zb, f.zEnd, f.active);
 }
 
 // Persistent warps over the tiles of [tile0, tile1) (a work queue: tiles
@@ -339,7 +511,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, 7)
     for (uint32_t tile = next_tile(&fb.counters[kCntTileQueue + 1], tile0); tile < tile1;
          tile = next_tile(&fb.counters[kCntTileQueue + 1], tile0)) {
         const uint2 tf = fb.tileFrag[tile];
-        views_tile(cam, tp, fb, vb, S, tile, tf.x, tf.y);
+        if (tf.y <= 32u) views_tile_small(cam, tp, fb, vb, S, tile, tf.x, tf.y);
+        else views_tile(cam, tp, fb, vb, S, tile, tf.x, tf.y);
         __syncwarp();
     }
 }

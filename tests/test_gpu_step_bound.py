@@ -39,7 +39,7 @@ def rd():
     r.close()
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1])  # the normals mode
 @pytest.mark.parametrize("name,w,h", [("C1", 0, 0), ("C2", 0, 0), ("C3", 0, 0), ("C5", 0, 0), ("random:64", 512, 512),
                                       ("gen:grid:2:mixed:smooth", 0, 0)])
 def test_view_local_bound_against_reference(rd, name, w, h, mode):
@@ -51,12 +51,12 @@ def test_view_local_bound_against_reference(rd, name, w, h, mode):
     rd.upload(s)
     evals = {}
     out = {}
-    for mode in (0, 1):
-        rd.set_step_bound(mode)
+    for sb in (0, 1):
+        rd.set_step_bound(sb)
         rd.reset_stats()
         rd.render_frame(s.device_camera, cfg, exact=False, graph=False)
-        out[mode] = rd.download_gbuffer()
-        evals[mode] = rd.stats().fieldEvals
+        out[sb] = rd.download_gbuffer()
+        evals[sb] = rd.stats().fieldEvals
     rd.set_step_bound(0)
     g = out[1]
     m = (gr.hit == 1) & (g.hit == 1)
