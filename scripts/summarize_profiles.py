@@ -36,6 +36,9 @@ KEYS = [
     ("sm__inst_executed_pipe_lsu.sum.pct_of_peak_sustained_active", "LSU pipe %"),
     ("sm__inst_executed_pipe_xu.sum.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
     ("sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "thread FFMA"),
+    ("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "thread FFMA (smsp)"),
+    ("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum", "thread FADD (smsp)"),
+    ("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", "thread FMUL (smsp)"),
     ("sm__sass_thread_inst_executed_op_fadd_pred_on.sum", "thread FADD"),
     ("sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "thread FMUL"),
     ("dram__bytes_read.sum", "DRAM bytes read"),
@@ -149,6 +152,10 @@ def main():
             traffic[kern] = {"dram_bytes_per_launch": rd_ * mul("dram__bytes_read.sum") + wr_ * mul("dram__bytes_write.sum"),
                              "duration_us": float(m.get("gpu__time_duration.sum", "nan")),
                              "source": f"profiles/{rnd}_{tag}_{kern}.md (ncu --set full)"}
+            fk = "smsp__sass_thread_inst_executed_op_%s_pred_on.sum"
+            if fk % "ffma" in m:  # executed FP32 flops per launch: 2 FFMA + FADD + FMUL (SURVEY 8(d) cross-check)
+                traffic[kern]["fp32_executed_flops"] = (2 * float(m[fk % "ffma"]) + float(m[fk % "fadd"]) +
+                                                        float(m[fk % "fmul"]))
         except (KeyError, ValueError):
             pass
     if traffic:
