@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--exact", action="store_true", help="IEEE-exact kernels instead of FMA field evaluation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--split", default="cost", choices=["cost", "even"],
+                    help="multi-GPU tile-row split: balanced by each row's march cost, or even row counts")
     return ap.parse_args()
 
 
@@ -239,8 +241,22 @@ class ShardedFrames:
         self.exact = bool(args.exact)
         self.W, self.H = self.scene.width, self.scene.height
         tiles_x, tiles_y = self.scene.tiles
-        # strong scaling: contiguous tile-row ranges per rank
+        # strong scaling: contiguous tile-row ranges per rank, balanced by the
+        # march cost of each row (the field evaluations of one full frame,
+        # computed on rank 0 and broadcast) -- the middle rows of a frame
+        # carry most of the surface; an even split leaves the edge ranks idle
         self.rows = tile_row_ranges(tiles_y, world)
+        if world > 1 and getattr(args, "split", "cost") == "cost":
+            import torch.distributed as dist
+
+            from paper_2304_09673_b200.distributed import row_costs
+            obj = [None]
+            if rank == 0:
+                self.rd.render_frame(self.cam, self.cfg, exact=self.exact, graph=False)
+                g = self.rd.download_gbuffer()
+                obj = [tile_row_ranges(tiles_y, world, row_costs(g.evalCount, self.W, self.H)).tolist()]
+            dist.broadcast_object_list(obj, src=0)
+            self.rows = np.asarray(obj[0], np.int64)
         self.tile0, self.tile1 = int(self.rows[rank] * tiles_x), int(self.rows[rank + 1] * tiles_x)
         if world == 1:
             self.tile0, self.tile1 = 0, 0
@@ -420,8 +436,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "config": bench_config(args.config, {
             "field_eval": "ieee-exact" if exact else "fma-contracted (tolerance path)",
             "l2": "flushed between timed frames (256 MiB device write, untimed)",
-            "parallelism": (f"tile rows over {world} GPU(s), "
-                            f"{'fused gather (IPC peer writes)' if fused else 'NCCL gather'}")
+            "parallelism": (f"tile rows over {world} GPU(s) ({args.split}-balanced split), "
+                            f"{'fused gather + per-rank normals (IPC peer memory)' if fused else 'NCCL gather'}")
                            if world > 1 else "1 GPU",
             "graph": f"{kernels.value} kernels / {nodes.value} nodes per frame"}),
         "gpu_launches": launches,

@@ -35,6 +35,18 @@ def tile_row_ranges(tiles_y: int, world: int, row_cost: np.ndarray | None = None
     return np.maximum.accumulate(np.clip(out, 0, tiles_y))
 
 
+def row_costs(eval_count: np.ndarray, width: int, height: int) -> np.ndarray:
+    """March cost of every tile row: the field evaluations of its pixels
+    (the G-buffer's evalCount plane of one full frame).  Feeding it to
+    tile_row_ranges balances the ranks' marches -- the frame's dominant
+    stage -- instead of their row counts."""
+    ev = np.asarray(eval_count, np.float64).reshape(height, width).sum(axis=1)
+    tiles_y = (height + 7) // 8
+    out = np.zeros(tiles_y, np.float64)
+    np.add.at(out, np.arange(height) // 8, ev)
+    return out
+
+
 def pixel_span(rows: np.ndarray, rank: int, width: int, height: int) -> tuple[int, int]:
     """[lo, hi) pixel-index range of rank's tile rows (row-major image)."""
     lo = int(min(rows[rank] * 8, height)) * width

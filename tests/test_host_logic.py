@@ -97,3 +97,16 @@ def test_gather_rows_gloo_world3(tmp_path):
     out = str(tmp_path / "result.txt")
     mp.spawn(_gather_worker, args=(3, _free_port(), out), nprocs=3, join=True)
     assert open(out).read() == "ok"
+
+
+def test_row_costs_balance_the_split():
+    """row_costs sums each tile row's evaluations; the cost-balanced split
+    puts more rows on the ranks whose rows are cheap."""
+    from paper_2304_09673_b200.distributed import row_costs
+    w, h = 64, 80  # 10 tile rows
+    ev = np.zeros((h, w), np.uint32)
+    ev[32:48, :] = 100  # tile rows 4 and 5 carry all the work
+    c = row_costs(ev.reshape(-1), w, h)
+    assert c.shape == (10,) and c[4] == c[5] == 100 * 8 * w and c.sum() == ev.sum()
+    rows = tile_row_ranges(10, 2, c)
+    assert rows[0] == 0 and rows[-1] == 10 and rows[1] == 5  # one heavy row per rank
