@@ -62,6 +62,7 @@ struct TileSmem {  // views pass, per warp
 // the min / max over the tile (warp reductions; finite values, order-free),
 // mapped to NDC once (ndc_from_view_z is monotone: bit for bit the
 // reference's per-ray min / max, two divisions per volume instead of two per ray).
+template <bool Fm>
 __device__ __forceinline__ bool raster_volume(const Cam& cam, const Voi& v, const float4* rays, float& entryOut,
                                               float& exitOut) {
     const RayVolPre pre = ray_vol_pre(v, cam.pos);  // the ray-independent terms, once per volume
@@ -77,23 +78,23 @@ __device__ __forceinline__ bool raster_volume(const Cam& cam, const Voi& v, cons
         if (v.family == 0u)
             hit = ray_sphere_pre(pre.a, pre.cc, d, t0, t1);
         else if (v.family == 1u)
-            hit = ray_obb_local(pre.a, d, v.rot, v.half, t0, t1);
+            hit = ray_obb_local<Fm>(pre.a, d, v.rot, v.half, t0, t1);
         else
-            hit = ray_capsule_pre(pre, d, t0, t1);
+            hit = ray_capsule_pre<Fm>(pre, d, t0, t1);
         if (!hit) continue;
         float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
         if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
         vz0 = smax(vz0, cam.nearZ);
         vz1 = smin(vz1, cam.farZ);
-        entry = smin(entry, vz0);
-        exitv = smax(exitv, vz1);
+        entry = tmin2<Fm>(entry, vz0);
+        exitv = tmax2<Fm>(exitv, vz1);
         any = true;
     }
     if (!__any_sync(kFull, any)) return false;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        entry = smin(entry, __shfl_xor_sync(kFull, entry, o));
-        exitv = smax(exitv, __shfl_xor_sync(kFull, exitv, o));
+        entry = tmin2<Fm>(entry, __shfl_xor_sync(kFull, entry, o));
+        exitv = tmax2<Fm>(exitv, __shfl_xor_sync(kFull, exitv, o));
     }
     entryOut = ndc_from_view_z(cam, entry);
     exitOut = ndc_from_view_z(cam, exitv);
@@ -105,6 +106,7 @@ __device__ __forceinline__ bool raster_volume(const Cam& cam, const Voi& v, cons
 // the (tile, volume) pairs ray-tested.
 constexpr uint32_t kCullList = 128;  // survivors of the tile cull kept per warp before the ray tests
 
+template <bool Fm>
 __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs& fb, uint32_t tile, int tx, int ty,
                                 int tilesX, uint32_t* list, float4* rays, uint4* sink, uint32_t sinkCap,
                                 uint32_t& tested) {
@@ -159,7 +161,7 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
             const uint32_t vk = list[i];
             const Voi v = vois[vk];
             float en, ex;
-            if (raster_volume(cam, v, rays, en, ex)) {
+            if (raster_volume<Fm>(cam, v, rays, en, ex)) {
                 if (lane == 0 && nf < sinkCap) sink[nf] = make_uint4(v.word, __float_as_uint(en), __float_as_uint(ex), vk);
                 ++nf;
             }
@@ -453,6 +455,9 @@ __device__ void views_tile_small(const Cam& cam, const TraceParams& tp, const Fr
 // differ by orders of magnitude in candidates and fragments).  Raster and
 // views are two kernels with their own register budgets (together in one
 // they spill); the views pass reads the tile's list back from L2.
+#ifndef BT_RASTER_FM
+#define BT_RASTER_FM 1
+#endif
 #ifndef BT_TILE_MINB
 #define BT_TILE_MINB 6  // CTAs per SM the register budget of k_tile_raster must fit
 #endif
@@ -462,6 +467,7 @@ __device__ __forceinline__ uint32_t next_tile(uint32_t* queue, uint32_t tile0) {
     return tile0 + __shfl_sync(kFull, q, 0);
 }
 
+template <bool Fm>
 __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
     k_tile_raster(Cam cam, const Voi* vois, FrameBufs fb, int tilesX, uint32_t tile0, uint32_t tile1) {
     __shared__ uint4 stage[kTileWarps][kTileStage];
@@ -478,7 +484,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
         uint32_t fbase = 0, nf = 0;
         if (!pairsLost) {
             uint32_t tested = 0;
-            nf = raster_tile(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], stage[wid], kTileStage, tested);
+            nf = raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], stage[wid], kTileStage, tested);
             testedSum += tested;
         }
         if (lane == 0 && nf) fbase = atomicAdd(&fb.counters[kCntFrags], nf);
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
             nf = 0;
         } else if (nf > kTileStage) {  // rare: too many fragments to sort in shared memory
             uint32_t tested = 0;
-            raster_tile(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], fb.unsorted + fbase, nf, tested);
+            raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], fb.unsorted + fbase, nf, tested);
             __syncwarp();
             sort_tile(fb.unsorted + fbase, nf, fb.frags + fbase);
         } else if (nf) {
@@ -533,9 +539,12 @@ void launch_tile_pass(cudaStream_t st, uint32_t mode, const Cam& cam, const Trac
     }
     if (tile1 <= tile0) return;
     const uint32_t want = (tile1 - tile0 + kTileWarps - 1) / kTileWarps;
-    if (mode & kTileRaster)
-        k_tile_raster<<<std::min<uint32_t>((uint32_t)smCount * BT_TILE_MINB, want), kTileWarps * 32, 0, st>>>(
-            cam, vois, fb, tilesX, tile0, tile1);
+    if (mode & kTileRaster) {
+        // FMNMX min / max where they are result-identical (bt_geom.cuh tmin2)
+        auto* k = (BT_RASTER_FM && cam.nearZ > 0.0f) ? k_tile_raster<true> : k_tile_raster<false>;
+        k<<<std::min<uint32_t>((uint32_t)smCount * BT_TILE_MINB, want), kTileWarps * 32, 0, st>>>(cam, vois, fb,
+                                                                                              tilesX, tile0, tile1);
+    }
     if (mode & kTileViews)
         k_tile_views<<<std::min<uint32_t>((uint32_t)smCount * 7u, want), kTileWarps * 32, 0, st>>>(cam, tp, fb, vb,
                                                                                                    tile0, tile1);
