@@ -15,6 +15,8 @@ constexpr uint32_t kScanBlockElems = 4096;  // elements per block of the single-
 
 struct DevTree {
     const float4* words = nullptr;
+    const uint32_t* blobs = nullptr;       // blob header of each node, indexed by its word (dense: the view
+                                           // build's ancestor walks read 4 B per node instead of a float4's .x)
     const uint32_t* primWords = nullptr;   // ascending word of each primitive
     const uint32_t* primOrd = nullptr;     // node ordinal of each primitive
     const uint32_t* nodeWord = nullptr;    // word of each node ordinal
@@ -164,12 +166,13 @@ void launch_copy_segments(cudaStream_t st, const void* const* src, void* const* 
 
 // ---- launchers (k_tree.cu) -------------------------------------------
 // compute_fast_indices on the device words (scratch: 4 n int32)
+void launch_blob_table(cudaStream_t st, const float4* words, const uint32_t* nodeWord, uint32_t n, uint32_t* blobs);
 void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWord, const int32_t* parentOrd,
                          uint32_t n, int32_t* scratch);
 
 // ---- launchers (k_views.cu) -------------------------------------------
 // k_view_build over the records k_tile allocated (thread per interval)
-void launch_view_build(cudaStream_t st, const DevTree& t, const ViewBufs& vb);
+void launch_view_build(cudaStream_t st, const DevTree& t, const ViewBufs& vb, int smCount);
 // longest-first march units of [tile0, tile1) from vb.tileCost (hist: 258 words of
 // scratch, [257] = unit count); tiles costing >= beta x the average work per
 // warp (at most cap of them) become two half-tile units

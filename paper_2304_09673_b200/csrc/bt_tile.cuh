@@ -18,18 +18,6 @@
 
 namespace btk {
 
-// float4 units of a view node's precomputed parameter block (tolerance
-// path, see bt_fast.cuh): affine rows for rotated primitives, reciprocals,
-// operator constants.
-BT_HD uint32_t fast_block_size(uint32_t blob) {
-    if (blob_is_prim(blob)) {
-        const uint32_t k = blob_op(blob);
-        return k == 0u ? 1u : k == 1u ? 5u : k == 2u ? 4u : k == 3u ? 4u : k == 4u ? 5u : 6u;
-    }
-    const uint32_t c = blob_op(blob);
-    return (c >= 6u && c <= 8u) ? 1u : (c >= 9u && c <= 11u) ? 2u : 0u;
-}
-
 // Tile error codes (tileError is 1 for either, like the reference's catch).
 constexpr uint32_t kErrStack = 1;
 constexpr uint32_t kErrView = 2;

@@ -49,7 +49,7 @@ struct ViewBufs {
     uint2* blockPrefix = nullptr;  // [scan blocks + 1], total at the end
     IntervalRec* iv = nullptr;     // [ivCap]
     uint2* nodes = nullptr;        // [nodeCap] (hdr, word)
-    uint32_t* counters = nullptr;  // [0] scan completion, [1] overflow flag
+    uint32_t* counters = nullptr;  // [1] overflow flag (see below)
     uint32_t* slab = nullptr;      // [tiles * slab stride] count-pass intervals (k_views.cu)
     const uint32_t* order = nullptr;  // optional march units in order (tile | kUnitSplit | kUnitPart1), else raster
     const uint32_t* unitCount = nullptr;  // number of entries of `order` (device)
@@ -295,7 +295,32 @@ struct WarpFetch {
 
 // ---------------------------------------------------------------- view build
 
-BT_DEV uint32_t tree_blob(const float4* words, uint32_t w) { return __float_as_uint(__ldg(&words[w].x)); }
+BT_DEV uint32_t tree_blob(const uint32_t* blobs, uint32_t w) { return __ldg(&blobs[w]); }
+
+// Per-node constants of a view entry, as packed-field lookups (a dynamically
+// indexed table would land in local memory):
+//   floats  parameters copied into the reference's cache (param_float_count,
+//           traversal.cpp:24-28): 7 transform floats + the shape's (sphere 1,
+//           ellipsoid 3, torus 2, box 3, sphere-cone 3, quadric 10); 2 for
+//           smooth / compact operators (field.hpp:106-116), 0 otherwise;
+//   blocks  float4s of the node's fast parameter block (convert_node,
+//           bt_fast.cuh): sphere 1, ellipsoid 5, torus 4, box 4, sphere-cone 5,
+//           quadric 6; smooth 1, compact 2;
+//   flops   SURVEY.md appendix-B weights: sphere 40, ellipsoid 57, torus 43,
+//           box 43, sphere-cone 52, quadric 85; smooth 8, compact 22.
+BT_HD void view_node_info(uint32_t blob, uint32_t& floats, uint32_t& blocks, uint32_t& flops) {
+    const uint32_t op = blob_op(blob);
+    if (blob_is_prim(blob)) {
+        floats = 7u + (op < 6u ? (0xA33231u >> (4u * op)) & 15u : 3u);  // shape floats 1 3 2 3 3 10
+        blocks = op < 5u ? (0x54451u >> (4u * op)) & 15u : 6u;           // 1 5 4 4 5, quadric 6
+        flops = op < 6u ? (uint32_t)((0x55342B2B3928ull >> (8u * op)) & 0xFFu) : 0u;  // 40 57 43 43 52 85
+    } else {
+        const bool smooth = op - 6u < 3u, compact = op - 9u < 3u;
+        floats = (smooth || compact) ? 2u : 0u;
+        blocks = smooth ? 1u : compact ? 2u : 0u;
+        flops = smooth ? 8u : compact ? 22u : 0u;
+    }
+}
 
 struct ViewOut {
     uint2* nodes;        // this view's node slots
@@ -309,19 +334,20 @@ BT_DEV void view_append(ViewOut& v, uint32_t blob, uint32_t word, bool copyParam
         v.err = kErrView;
         return;
     }
-    const uint32_t floats = copyParams ? param_floats(blob) : 0u;
+    uint32_t floats, blocks, flops;
+    view_node_info(blob, floats, blocks, flops);
+    if (!copyParams) floats = 0u;
     if (floats > 0u && v.cacheFloats + floats <= kCacheFloats) v.cacheFloats += floats;
     v.nodes[v.nView] = make_uint2((blob & 0xFC000000u) | (v.nBlocks << 4), word);  // byte offset of the block
-    v.nBlocks += fast_block_size(blob);
+    v.nBlocks += blocks;
     v.nView++;
-    // evaluation stack depth and appendix-B flops of one evaluation
+    v.flops += flops;  // appendix-B flops of one evaluation
+    // evaluation stack depth
     if (blob_is_prim(blob)) {
         v.depth++;
         v.maxDepth = v.depth > v.maxDepth ? v.depth : v.maxDepth;
-        v.flops += prim_flops(blob_op(blob));
     } else {
         v.depth--;
-        v.flops += op_flops(blob_op(blob));
     }
 }
 
@@ -329,77 +355,114 @@ BT_DEV void view_append(ViewOut& v, uint32_t blob, uint32_t word, bool copyParam
 // traversal.cpp:30-99) over the n active words (ascending), which sit in the
 // .x of v.nodes[n - 1 + i]; the view is written over the same 2n - 1 slots
 // (node m goes to slot m <= 2i + 1 < n - 1 + (i + 1) while active i + 1 is
-// still unread).  Returns rootUsed.
-BT_DEV uint32_t build_view_inplace(ViewOut& v, uint32_t n, const float4* words) {
-    v.nView = v.nPrim = v.nBlocks = v.cacheFloats = v.depth = v.maxDepth = v.err = 0;
-    v.flops = 12u;
-    if (n == 0) return 0u;
-    v.capacity = 2u * n - 1u;
-    const uint2* act2 = v.nodes + (n - 1u);
-    uint32_t sBlob[kStackCap];
-    uint8_t sUse[kStackCap];
-    uint32_t sp = 0;
-    for (uint32_t i = 0; i < n && !v.err; ++i) {
-        const uint32_t w = act2[i].x;
-        uint32_t nodeBlob = tree_blob(words, w);
-        view_append(v, nodeBlob, w, true);  // visitor.primitive
-        v.nPrim++;
-        uint32_t data = 1u;
-        if (sp > 0) nodeBlob = blob_with_anc(nodeBlob, min(blob_anc(nodeBlob), blob_anc(sBlob[sp - 1])));
-        const uint32_t nextAct = (i + 1 < n) ? act2[i + 1].x : 0u;
-        for (;;) {
-            const uint32_t anc = blob_anc(nodeBlob);
-            const bool shadowed = (i + 1 < n) && anc > nextAct;
-            const bool lastDone = (i + 1 == n) && (sp == 0 && anc == kSentinel);
-            if (shadowed || lastDone) break;
-            if (anc == kSentinel) {  // "traversal walked past the root"
-                v.err = kErrLogic;
-                return 0u;
-            }
-            const uint32_t opWord = anc;
-            const bool fromLeft = blob_is_left(nodeBlob);
-            nodeBlob = tree_blob(words, opWord);
-            bool combined = false;
-            if (sp > 0) {
-                const uint32_t cb = sBlob[sp - 1];
-                const uint32_t ca = blob_anc(cb), na = blob_anc(nodeBlob);
-                const bool pop = (opWord == ca) || (na >= ca && (na == kSentinel || blob_is_left(nodeBlob)));
-                if (pop) {
-                    // visitor.combine(left = stacked, right = current)
-                    const uint32_t children = ((uint32_t)sUse[sp - 1] << 1) | data;
-                    const uint32_t opType = ((~children & blob_ignore(nodeBlob)) & 3u) == 0u ? children : 0u;
-                    uint32_t stored = nodeBlob;
-                    if (opType != 3u) stored = blob_with_op(stored, opType);
-                    view_append(v, stored, opWord, opType == 3u);
-                    data = opType != 0u ? 1u : 0u;
-                    --sp;
-                    combined = true;
-                }
-            }
-            if (!combined) {
-                // visitor.pass: selector nodes only gate the usage bit
-                const uint32_t mask = fromLeft ? 1u : 2u;
-                if (blob_ignore(nodeBlob) & mask) data = 0u;
-            }
-            if (sp > 0) nodeBlob = blob_with_anc(nodeBlob, min(blob_anc(nodeBlob), blob_anc(sBlob[sp - 1])));
-        }
-        if (v.err) return 0u;
-        if (sp >= kStackCap) {
-            v.err = kErrStack;
-            return 0u;
-        }
-        sBlob[sp] = nodeBlob;
-        sUse[sp] = (uint8_t)data;
-        ++sp;
+// still unread).
+//
+// Restated as a state machine that advances ONE node dereference per call
+// (one loop, not the reference's nested primitive / walk loops), with the
+// next primitive's word and blob read one primitive ahead, off the walk's
+// pointer-chasing chain.  The traversal stack lives in shared memory, one u32
+// per entry: a stacked node is only ever consulted for its ancestor
+// (pop_required, the min() of traversal.hpp:92,110) and its usage bit, so
+// entry = ancestor | usage << 31.  Errors end the view at once: the reference
+// throws, and every later step of the loop would leave the record unchanged
+// (view_append is a no-op once err is set).
+struct ViewBuild {
+    ViewOut v;
+    const uint2* act2;
+    uint32_t n, i, sp, nodeBlob, data, nextAct;
+    uint32_t w0, b0, w1;  // read ahead: the next primitive's word and blob, and the word after it
+    bool start;      // the next step begins active primitive i
+    bool done;
+    uint32_t rootUsed;
+
+    BT_DEV void begin(uint2* nodes, uint32_t count, const uint32_t* blobs) {
+        v.nodes = nodes;
+        v.nView = v.nPrim = v.nBlocks = v.cacheFloats = v.depth = v.maxDepth = v.err = 0;
+        v.flops = 12u;
+        v.capacity = count ? 2u * count - 1u : 0u;
+        n = count;
+        act2 = nodes + (count ? count - 1u : 0u);
+        i = sp = 0;
+        nodeBlob = data = 0;
+        nextAct = 0u;
+        w0 = count ? act2[0].x : 0u;
+        b0 = count ? tree_blob(blobs, w0) : 0u;
+        w1 = count > 1u ? act2[1].x : 0u;
+        start = true;
+        rootUsed = 0;
+        done = count == 0u;
     }
-    if (v.err) return 0u;
-    const uint32_t result = sUse[sp - 1];
-    --sp;
-    if (sp != 0) {
-        v.err = kErrLogic;
-        return 0u;
+    BT_DEV void fail(uint32_t e) {
+        if (!v.err) v.err = e;
+        rootUsed = 0;
+        done = true;
     }
-    return result;
-}
+    // stk[k * stride]: entry k of this thread's stack
+    BT_DEV void step(const uint32_t* blobs, uint32_t* stk, uint32_t stride) {
+        if (start) {  // visitor.primitive: active i (w0, b0) and i + 1 (w1) were read ahead
+            const uint32_t w = w0;
+            nodeBlob = b0;
+            view_append(v, nodeBlob, w, true);
+            v.nPrim++;
+            data = 1u;
+            if (sp > 0) nodeBlob = blob_with_anc(nodeBlob, min(blob_anc(nodeBlob), stk[(sp - 1) * stride] & kSentinel));
+            nextAct = (i + 1 < n) ? w1 : 0u;
+            // read ahead, off the walk's dependency chain: active i + 1's blob, active i + 2's word
+            // (slot n + 1 + i: only slots <= 2i have been written so far)
+            if (i + 1 < n) {
+                w0 = w1;
+                b0 = tree_blob(blobs, w1);
+            }
+            if (i + 2 < n) w1 = act2[i + 2].x;
+            start = false;
+        }
+        if (v.err) return fail(v.err);
+        const uint32_t anc = blob_anc(nodeBlob);
+        const bool shadowed = (i + 1 < n) && anc > nextAct;
+        const bool lastDone = (i + 1 == n) && (sp == 0 && anc == kSentinel);
+        if (shadowed || lastDone) {  // the walk of primitive i ends: push
+            if (sp >= kStackCap) return fail(kErrStack);
+            stk[sp * stride] = anc | (data << 31);
+            ++sp;
+            if (++i < n) {
+                start = true;
+                return;
+            }
+            const uint32_t result = stk[(sp - 1) * stride] >> 31;
+            if (--sp != 0) return fail(kErrLogic);  // "traversal left values on the stack"
+            rootUsed = result;
+            done = true;
+            return;
+        }
+        if (anc == kSentinel) return fail(kErrLogic);  // "traversal walked past the root"
+        const uint32_t opWord = anc;
+        const bool fromLeft = blob_is_left(nodeBlob);
+        nodeBlob = tree_blob(blobs, opWord);
+        bool combined = false;
+        if (sp > 0) {
+            const uint32_t top = stk[(sp - 1) * stride];
+            const uint32_t ca = top & kSentinel, na = blob_anc(nodeBlob);
+            const bool pop = (opWord == ca) || (na >= ca && (na == kSentinel || blob_is_left(nodeBlob)));
+            if (pop) {
+                // visitor.combine(left = stacked, right = current)
+                const uint32_t children = ((top >> 31) << 1) | data;
+                const uint32_t opType = ((~children & blob_ignore(nodeBlob)) & 3u) == 0u ? children : 0u;
+                uint32_t stored = nodeBlob;
+                if (opType != 3u) stored = blob_with_op(stored, opType);
+                view_append(v, stored, opWord, opType == 3u);
+                data = opType != 0u ? 1u : 0u;
+                --sp;
+                combined = true;
+            }
+        }
+        if (!combined) {
+            // visitor.pass: selector nodes only gate the usage bit
+            const uint32_t mask = fromLeft ? 1u : 2u;
+            if (blob_ignore(nodeBlob) & mask) data = 0u;
+        }
+        if (sp > 0) nodeBlob = blob_with_anc(nodeBlob, min(blob_anc(nodeBlob), stk[(sp - 1) * stride] & kSentinel));
+        if (v.err) fail(v.err);
+    }
+};
 
 }  // namespace btk

@@ -97,7 +97,7 @@ struct bt_ctx {
 
     // tree
     DevBuf<float4> words;
-    DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram;
+    DevBuf<uint32_t> primWords, primOrd, nodeWord, fullProgram, upperProgram, blobs;
     DevBuf<uint2> frontier;
     uint32_t nFrontier = 0, nUpper = 0, upperIsChain = 0, upperIsMinChain = 0;
     DevBuf<int32_t> compactAnc, parentOrd, fastScratch;
@@ -206,6 +206,7 @@ struct DevGuard {
 DevTree dev_tree(const bt_ctx* c) {
     DevTree t;
     t.words = c->words.ptr;
+    t.blobs = c->blobs.ptr;
     t.primWords = c->primWords.ptr;
     t.primOrd = c->primOrd.ptr;
     t.nodeWord = c->nodeWord.ptr;
@@ -605,7 +606,7 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         BT_CUDA(cudaEventRecord(c->evJoin[1], c->side));
     }
     if (prof) cudaEventRecord(c->ev[4], c->stream);
-    launch_view_build(c->stream, t, view_bufs(c));
+    launch_view_build(c->stream, t, view_bufs(c), c->smCount);
     if (prof) cudaEventRecord(c->ev[5], c->stream);
     if (forkOrder) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[1], 0));
     ViewBufs vbm = view_bufs(c);
@@ -705,7 +706,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->graph) cudaGraphExecDestroy(c->graph);
     c->frontier.release();
-    for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->upperProgram, &c->pWords, &c->pCounts,
+    for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->upperProgram, &c->blobs, &c->pWords, &c->pCounts,
                     &c->tileCount, &c->tileCursor, &c->tileLocal, &c->blockSum, &c->blockPrefix, &c->offsets,
                     &c->counters, &c->evalCount, &c->tileMaxOverlap, &c->tileCacheBytes, &c->fallback})
         b->release();
@@ -813,6 +814,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
         std::memcmp(c->hostPrimWords.data(), primitiveWords, (size_t)nprims * 4) == 0) {
         // same structure: the side tables stay valid, only parameters changed
         BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
+        launch_blob_table(c->stream, c->words.ptr, c->nodeWord.ptr, nnodes, c->blobs.ptr);
         BT_CUDA(cudaStreamSynchronize(c->stream));
         c->haveRoi = false;
         c->nvoi = 0;
@@ -918,6 +920,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(c->primWords.reserve(nprims));
     BT_CUDA(c->primOrd.reserve(nprims));
     BT_CUDA(c->nodeWord.reserve(nnodes));
+    BT_CUDA(c->blobs.reserve(nwords));
     BT_CUDA(c->compactAnc.reserve(nnodes));
     BT_CUDA(c->parentOrd.reserve(nnodes));
     BT_CUDA(c->fullProgram.reserve(nnodes));
@@ -930,6 +933,8 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(cudaMemcpyAsync(c->primWords.ptr, primitiveWords, nprims * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->primOrd.ptr, primOrd.data(), nprims * 4, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->nodeWord.ptr, nodeWord.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
+    BT_CUDA(cudaMemsetAsync(c->blobs.ptr, 0, (size_t)nwords * 4, c->stream));
+    launch_blob_table(c->stream, c->words.ptr, c->nodeWord.ptr, nnodes, c->blobs.ptr);
     BT_CUDA(cudaMemcpyAsync(c->compactAnc.ptr, compactAnc.data(), nnodes * 4, cudaMemcpyHostToDevice, c->stream));
     c->haveAncLists = ancLists;
     if (ancLists) {
@@ -978,6 +983,7 @@ int bt_tree_fast_indices(bt_ctx* c) {
     if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
     BT_CUDA(c->fastScratch.reserve((size_t)c->nnodes * 4));
     launch_fast_indices(c->stream, c->words.ptr, c->nodeWord.ptr, c->parentOrd.ptr, c->nnodes, c->fastScratch.ptr);
+    launch_blob_table(c->stream, c->words.ptr, c->nodeWord.ptr, c->nnodes, c->blobs.ptr);
     BT_CUDA(cudaGetLastError());
     return BT_OK;
 }

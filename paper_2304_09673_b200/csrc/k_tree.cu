@@ -56,7 +56,19 @@ __global__ void k_fast_write(float4* words, const uint32_t* nodeWord, const int3
     w->x = __uint_as_float(blob_with_anc(b, nodeWord[target]));
 }
 
+// the dense blob table (DevTree::blobs): every node's header word, at its word
+__global__ void k_blob_table(const float4* words, const uint32_t* nodeWord, uint32_t n, uint32_t* blobs) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t w = nodeWord[i];
+    blobs[w] = __float_as_uint(words[w].x);
+}
+
 }  // namespace
+
+void launch_blob_table(cudaStream_t st, const float4* words, const uint32_t* nodeWord, uint32_t n, uint32_t* blobs) {
+    if (n) k_blob_table<<<(n + 255) / 256, 256, 0, st>>>(words, nodeWord, n, blobs);
+}
 
 void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWord, const int32_t* parentOrd,
                          uint32_t n, int32_t* scratch) {
