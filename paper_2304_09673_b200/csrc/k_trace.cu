@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "bt_bulk.cuh"
 #include "bt_device.h"
 #include "bt_fast.cuh"
 #include "bt_views.cuh"
@@ -71,7 +72,7 @@ __device__ unsigned int g_stepDone;
 // Per-warp shared memory of k_march.
 struct MarchSmem {
     float4 blocks[kMarchBlocks];  // fast parameter blocks of the staged view
-    float4 rays[64];              // dir.xyz, dot(dir, forward) of the tile's rays
+    float4 rays[64];              // dir.xyz, dot(dir, forward) of the tile's rays (one bulk copy)
     uint32_t hdr[kViewCap];       // staged view: isPrim(1) op(5) | block byte offset
     union {
         uint32_t word[kViewCap + 1];      // exact path / raw parameters: tree word of each node
@@ -84,6 +85,7 @@ struct MarchSmem {
     // per-tile accounting, kept here rather than in registers live across the march
     uint32_t accFe[32], accFl[32], accRnv[32], accPe[32];
     uint32_t tileMaxOv, tileCache, tileErr, steps;
+    uint64_t rayBar;              // completion barrier of the rays' bulk copy
 };
 
 // Per-block work accounting, flushed to the device statistics once per CTA.
@@ -136,8 +138,12 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
                     ray = s.pend[rank];
                     const float4 r = s.rays[ray];
                     dir = F3{r.x, r.y, r.z};
-                    if (IsFast<O>::value) march_begin(m, vz0 * r.w, vz1 * r.w);  // r.w = 1 / dot(dir, forward)
-                    else march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w));
+                    if (IsFast<O>::value) {  // t = view z * (1 / dot(dir, forward))
+                        const float iw = FastOps::rcp(r.w);
+                        march_begin(m, vz0 * iw, vz1 * iw);
+                    } else {
+                        march_begin(m, E::div(vz0, r.w), E::div(vz1, r.w));
+                    }
                 }
                 cursor += __popc(idleMask);
             }
@@ -186,7 +192,7 @@ __device__ __forceinline__ void unit_rays(const GBuf& g, int tx, int ty, uint32_
 template <class O, bool SB = false>
 __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, const TraceParams& tp,
                                            const FrameBufs& fb, const ViewBufs& vb, const GBuf& g, MarchSmem& s,
-                                           BlockStats& bs, int lane, uint32_t unit) {
+                                           BlockStats& bs, int lane, uint32_t unit, uint32_t& rayPhase) {
     const uint32_t lt = lanemask_lt();
     // a unit is a whole tile, or half of one (the rays of one pixel-column parity)
     const uint32_t tile = unit & kUnitTile;
@@ -204,13 +210,11 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
     if (c.x != 0u && vb.counters[1] != 0u) {
         if (lane == 0) s.tileErr = 1;  // interval records overflowed in a graph replay (flagged to the host)
     } else if (c.x != 0u) {
+        // the tile's 64 rays: one 1 KB bulk copy (tile-major ray layout)
+        if (lane == 0) bulk_load(s.rays, fb.rays + (size_t)tile * 64, 64 * sizeof(float4), &s.rayBar);
         const uint2 o = view_offset(vb, tile);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            float4 r = fb.rays[(size_t)tile * 64 + lane + 32 * j];
-            if (IsFast<O>::value) r.w = FastOps::rcp(r.w);  // t = view z * (1 / dot(dir, forward))
-            s.rays[lane + 32 * j] = r;
-        }
+        mbar_wait(&s.rayBar, rayPhase);
+        rayPhase ^= 1u;
         for (uint32_t k = 0; k < c.x; ++k) {
             uint32_t v0, v1;
             unit_rays(g, tx, ty, mine, v0, v1);
@@ -360,6 +364,9 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
     if (threadIdx.x == 0) bs = BlockStats{0, 0, 0, 0, 0, 0, 0u, 0u};
     __syncthreads();
     MarchSmem& s = smem[wid];
+    if (lane == 0) mbar_init(&s.rayBar);
+    __syncwarp();
+    uint32_t rayPhase = 0;
     const uint32_t nUnits = vb.order ? *vb.unitCount : tile1 - tile0;
     for (;;) {
         uint32_t q = 0;
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(kTraceWarps * 32, MinBlocks)
         q = __shfl_sync(kFull, q, 0);
         if (q >= nUnits) break;
         const uint32_t tile = vb.order ? vb.order[q] : tile0 + q;
-        march_tile<O, SB>(t, cam, tp, fb, vb, g, s, bs, lane, tile);
+        march_tile<O, SB>(t, cam, tp, fb, vb, g, s, bs, lane, tile, rayPhase);
     }
     // fused gather: this rank's pixels went to another GPU's planes; make
     // them visible system-wide before the kernel ends (the completion

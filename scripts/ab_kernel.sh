@@ -1,15 +1,19 @@
-# A/B of one kernel's device time across library variants (lib/ab/lib<V>.so from
+# A/B of kernels' device time across library variants (lib/ab/lib<V>.so from
 # scripts/build_variant.sh): ncu launch list (cold-cache, serialised) per
-# variant and config, mean us per launch of the kernels matching $KERN.
-#   usage: VARS="A B" CFGS="C3 C5" KERN=k_view_build bash scripts/ab_kernel.sh
+# variant and config, mean us per launch of the kernels matching $KERN (a
+# regex), skipping the first two launches.  FRAMES=1 profiles whole bench
+# frames (bench.py) instead of march_bench.py's stage-(c) repeats.
+#   usage: VARS="A B" CFGS="C3 C5" KERN="k_view_build|k_march" bash scripts/ab_kernel.sh
 LIB=paper_2304_09673_b200/lib/libblobtree_b200.so
 cp $LIB /tmp/lib_current.so
 mkdir -p gpurun_out
 for v in ${VARS:-A B}; do
   cp paper_2304_09673_b200/lib/ab/lib$v.so $LIB
   for cfg in ${CFGS:-C3 C5}; do
-    timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${KERN:-k_march} -c 12 --csv \
-      --log-file gpurun_out/ab_${v}_${cfg}.csv python scripts/march_bench.py $cfg 3 > /dev/null 2>&1
+    if [ -n "$FRAMES" ]; then CMD="python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline --no-sweep"
+    else CMD="python scripts/march_bench.py $cfg 3"; fi
+    timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:${KERN:-k_march}" -c ${NLAUNCH:-12} --csv \
+      --log-file gpurun_out/ab_${v}_${cfg}.csv $CMD > /dev/null 2>&1
     python - "$v" "$cfg" gpurun_out/ab_${v}_${cfg}.csv <<'PY'
 import csv, sys, collections
 agg = collections.defaultdict(list)
