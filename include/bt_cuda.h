@@ -279,6 +279,17 @@ BT_API int bt_set_scheduling(bt_ctx* ctx, int mode);
  * held to its own tolerance contract against the reference
  * (tests/test_gpu_step_bound.py), never to bit-exactness. */
 BT_API int bt_set_step_bound(bt_ctx* ctx, int mode);
+/* Depth slabs (extension, PAPER.md "Conclusion and Future work": "when
+ * targeting higher resolution, using larger tiles and processing by depth
+ * slabs could also limit memory usage").  slabs > 1: bt_render_frame cuts
+ * the view depth [near, far] into `slabs` equal slabs and builds the A-buffer,
+ * the interval records and the march one slab at a time, front to back; a ray
+ * that hits in a slab is done, the others continue in the next.  The A-buffer
+ * and record buffers then hold one slab's fragments.  Fragments crossing a
+ * slab boundary are clipped to it, so the march restarts there: held to its
+ * own tolerance contract against the reference (tests/test_gpu_depth_slabs.py),
+ * never to bit-exactness.  1 (default): the reference's single pass. */
+BT_API int bt_set_depth_slabs(bt_ctx* ctx, int slabs);
 BT_API int bt_set_tile_order(bt_ctx* ctx, const uint32_t* order, uint32_t n);
 BT_API int bt_gbuffer_device(bt_ctx* ctx, bt_gbuffer_view* out);
 /* hit/depth planes from the host (compute_normals on a caller's G-buffer) */

@@ -108,6 +108,7 @@ PROTOTYPES = {
     "bt_gbuffer_import_release": [vp],
     "bt_set_scheduling": [vp, C.c_int],
     "bt_set_step_bound": [vp, C.c_int],
+    "bt_set_depth_slabs": [vp, C.c_int],
     "bt_gbuffer_device": [vp, P(bt_gbuffer_view)],
     "bt_gbuffer_upload": [vp, P(bt_camera), vp, vp],
     "bt_stats_download": [vp, P(bt_stats)],

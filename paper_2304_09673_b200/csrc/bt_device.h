@@ -112,6 +112,7 @@ struct GBuf {
     uint32_t* fallback = nullptr;  // pixel indices needing the gradient normal
     int width = 0, height = 0, tilesX = 0, tilesY = 0;
     int remote = 0;  // the planes are another GPU's (fused gather): fence the writes system-wide
+    int accumulate = 0;  // depth slab > 0: the march continues the planes of the earlier slabs
 };
 
 inline Cam make_cam(const float* pos, const float* fwd, const float* right, const float* up,

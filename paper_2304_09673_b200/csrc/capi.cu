@@ -164,6 +164,7 @@ struct bt_ctx {
     bool viewsFrame = false;  // the G-buffer came from a whole-frame FMA-path march (its records are valid)
     int schedMode = 1;
     int stepBound = 0;  // 0 reference (global L), 1 view-local Lipschitz bound (bt_set_step_bound)
+    int depthSlabs = 1;  // > 1: frames rendered slab by slab in view depth (bt_set_depth_slabs)
     DevBuf<uint32_t> tileQueue;   // k_trace work queue head
     DevBuf<float> gradScratch;  // per-warp primitive values of the gradient fallback
     uint32_t gradWarps = 0;
@@ -570,8 +571,11 @@ float split_beta() {
 // march.  In `checked` mode the record totals are read back and the buffers
 // grown (2x headroom); inside a graph replay an overflow is flagged
 // (bt_stats_download) and the tiles marked.
+// `slab` >= 0: depth slab `slab` of a slab-by-slab frame (cam = the slab's
+// camera, `window` the frame camera's fetch window; slabs after the first
+// continue the G-buffer of the earlier ones, in raster order).
 int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint32_t tile0, uint32_t tile1,
-             int exact, bool checked, bool haveRecords = false) {
+             int exact, bool checked, bool haveRecords = false, int slab = -1, float window = 0.0f) {
     if (c->tileQueue.cap == 0) {
         BT_CUDA(c->tileQueue.reserve(1));
         c->bufEpoch++;
@@ -579,7 +583,8 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     const uint32_t tiles = (uint32_t)(c->tilesX * c->tilesY);
     const DevTree t = dev_tree(c);
     const Cam k = to_cam(cam);
-    const TraceParams tp = trace_params(cfg, cam, c->stepBound);
+    TraceParams tp = trace_params(cfg, cam, c->stepBound);
+    if (slab >= 0) tp.window = window;
     // stage events only in eager frames: synchronising on an event inside a
     // stream capture would invalidate the capture
     const bool prof = c->profiling && checked;
@@ -594,8 +599,11 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         launch_tile_order(st, view_bufs(c), trace_gbuf(c), c->orderHist.ptr, c->tileOrder.ptr, tile0, tile1,
                           trace_grid_warps(c->smCount), split_beta(), 2u * trace_grid_warps(c->smCount));
     };
-    const bool forkOrder = c->schedMode == 1 && !checked;
-    if (c->schedMode == 1 && checked) order(c->stream);
+    // (a slab frame keeps raster order: the half-tile split would reset the
+    // tile planes the earlier slabs wrote)
+    const int sched = slab >= 0 ? 0 : c->schedMode;
+    const bool forkOrder = sched == 1 && !checked;
+    if (sched == 1 && checked) order(c->stream);
     if (prof) cudaEventRecord(c->ev[3], c->stream);
     if (forkOrder) {
         int rc = ensure_side(c);
@@ -610,15 +618,17 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
     if (prof) cudaEventRecord(c->ev[5], c->stream);
     if (forkOrder) BT_CUDA(cudaStreamWaitEvent(c->stream, c->evJoin[1], 0));
     ViewBufs vbm = view_bufs(c);
-    if (c->schedMode == 1) {
+    if (sched == 1) {
         vbm.order = c->tileOrder.ptr;
         vbm.unitCount = c->orderHist.ptr + 257;
-    } else if (c->schedMode == 2 && tile0 == 0 && tile1 == tiles) {
+    } else if (sched == 2 && tile0 == 0 && tile1 == tiles) {
         vbm.order = c->tileOrder.ptr;
         vbm.unitCount = c->hostUnits.ptr;
     }
-    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, trace_gbuf(c), c->stats.ptr, tile0, tile1,
-                 c->smCount, c->tileQueue.ptr, !c->prezeroed);
+    GBuf gm = trace_gbuf(c);
+    gm.accumulate = slab > 0 ? 1 : 0;
+    launch_trace(c->stream, exact != 0, t, k, tp, frame_bufs(c), vbm, gm, c->stats.ptr, tile0, tile1, c->smCount,
+                 c->tileQueue.ptr, !c->prezeroed || slab > 0);
     if (prof) {  // sub-stage split: views (records, build) and the march alone
         cudaEventRecord(c->ev[1], c->stream);
         cudaEventSynchronize(c->ev[1]);
@@ -632,8 +642,22 @@ int do_trace(bt_ctx* c, const bt_camera& cam, const bt_render_config& cfg, uint3
         c->profLaunch[5] += 1;
     }
     c->haveGbuffer = true;
-    c->viewsFrame = !exact && tile0 == 0 && tile1 == tiles;
+    // (a slab frame's records cover its last slab only: normals' fallback over the full tree)
+    c->viewsFrame = !exact && tile0 == 0 && tile1 == tiles && slab < 0;
     return BT_OK;
+}
+
+// The camera of depth slab s of n: view depth [near, far] cut into n equal
+// slabs; the A-buffer of a slab clips its fragments to the slab (rasterize_
+// volumes' near / far clip), and its NDC constants are the slab's own.
+bt_camera slab_camera(const bt_camera& cam, int s, int n) {
+    bt_camera k = cam;
+    const float range = cam.farZ - cam.nearZ;
+    k.nearZ = s == 0 ? cam.nearZ : cam.nearZ + range * (float)s / (float)n;
+    k.farZ = s == n - 1 ? cam.farZ : cam.nearZ + range * (float)(s + 1) / (float)n;
+    k.invNear = 1.0f / k.nearZ;
+    k.invDepthRange = 1.0f / (k.invNear - 1.0f / k.farZ);
+    return k;
 }
 
 // rows [y0, y1) of the image (y1 < 0: all); `target`: the planes to shade
@@ -1347,10 +1371,26 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
         if (r) return r;
         // one per-tile pass builds each tile's fragment list AND its interval records
         const TraceParams tp = trace_params(*cfg, *cam, c->stepBound);
-        r = do_abuffer(c, *cam, tile0, tile1, checked, kTileRaster | kTileViews, &tp);
-        if (r) return r;
-        r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked, true);
-        if (r) return r;
+        if (c->depthSlabs <= 1) {
+            r = do_abuffer(c, *cam, tile0, tile1, checked, kTileRaster | kTileViews, &tp);
+            if (r) return r;
+            r = do_trace(c, *cam, *cfg, tile0, tile1, exact, checked, true);
+            if (r) return r;
+        } else {
+            // depth slabs (PAPER.md "Conclusion": processing by depth slabs limits
+            // the A-buffer's memory): A-buffer, records and march per slab, front
+            // to back; rays that hit stay done
+            for (int sl = 0; sl < c->depthSlabs; ++sl) {
+                const bt_camera cs = slab_camera(*cam, sl, c->depthSlabs);
+                TraceParams tps = trace_params(*cfg, cs, c->stepBound);
+                tps.window = tp.window;
+                if (sl > 0) c->prezeroed = false;  // the frame's counters, again for this slab
+                r = do_abuffer(c, cs, tile0, tile1, checked, kTileRaster | kTileViews, &tps);
+                if (r) return r;
+                r = do_trace(c, cs, *cfg, tile0, tile1, exact, checked, true, sl, tp.window);
+                if (r) return r;
+            }
+        }
         return normals ? do_normals(c, *cam, mode, exact) : BT_OK;
     };
     if (!use_graph) {
@@ -1595,6 +1635,17 @@ int bt_set_step_bound(bt_ctx* c, int mode) {
     if (mode != 0 && mode != 1) return fail(BT_EINVAL, "step bound mode must be 0 or 1");
     if (mode != c->stepBound) {
         c->stepBound = mode;
+        c->bufEpoch++;  // re-capture the frame graph
+    }
+    return BT_OK;
+}
+
+int bt_set_depth_slabs(bt_ctx* c, int slabs) {
+    DevGuard dg_(c);
+    if (!c) return fail(BT_EINVAL, "ctx is null");
+    if (slabs < 1 || slabs > 64) return fail(BT_EINVAL, "depth slabs must lie in [1, 64]");
+    if (slabs != c->depthSlabs) {
+        c->depthSlabs = slabs;
         c->bufEpoch++;  // re-capture the frame graph
     }
     return BT_OK;

@@ -199,10 +199,23 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
     const bool half = (unit & kUnitSplit) != 0u;
     const uint32_t mine = !half ? kFull : ((unit & kUnitPart1) ? 0xAAAAAAAAu : 0x55555555u);
     const int tx = (int)(tile % (uint32_t)g.tilesX), ty = (int)(tile / (uint32_t)g.tilesX);
-    s.hit[lane] = 0;
-    s.hit[lane + 32] = 0;
-    s.evals[lane] = 0;
-    s.evals[lane + 32] = 0;
+    if (g.accumulate) {  // a later depth slab: the rays that hit in an earlier one are done
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int li = lane + 32 * j;
+            const int px = tx * kTile + (li & 7), py = ty * kTile + (li >> 3);
+            const bool in = px < g.width && py < g.height;
+            const size_t p = in ? (size_t)py * g.width + px : 0;
+            s.hit[li] = in ? g.hit[p] : 0;
+            s.depth[li] = in ? g.depth[p] : 0.0f;
+            s.evals[li] = in ? g.evalCount[p] : 0u;
+        }
+    } else {
+        s.hit[lane] = 0;
+        s.hit[lane + 32] = 0;
+        s.evals[lane] = 0;
+        s.evals[lane + 32] = 0;
+    }
     s.accFe[lane] = s.accFl[lane] = s.accRnv[lane] = s.accPe[lane] = 0;
     if (lane == 0) s.tileMaxOv = s.tileCache = s.tileErr = s.steps = 0;
     __syncwarp();
@@ -325,10 +338,14 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
     if (lane == 0) {
         const uint32_t tileMaxOv = s.tileMaxOv, tileCache = s.tileCache;
         uint32_t tileErr = s.tileErr;
-        if (!half) {
+        if (!half && !g.accumulate) {
             g.tileMaxOverlap[tile] = tileMaxOv;
             g.tileCacheBytes[tile] = tileCache;
             g.tileError[tile] = (uint8_t)tileErr;
+        } else if (!half) {  // a later depth slab: the tile's planes over all slabs
+            g.tileMaxOverlap[tile] = max(g.tileMaxOverlap[tile], tileMaxOv);
+            g.tileCacheBytes[tile] = max(g.tileCacheBytes[tile], tileCache);
+            if (tileErr) g.tileError[tile] = 1;
         } else {  // both halves walk a prefix of the same intervals: the tile's values are the max
             if (tileMaxOv) atomicMax(&g.tileMaxOverlap[tile], tileMaxOv);
             if (tileCache) atomicMax(&g.tileCacheBytes[tile], tileCache);

@@ -291,6 +291,11 @@ class Renderer:
         view (1-Lipschitz views march with L = 1; bt_set_step_bound)."""
         check(self.lib.bt_set_step_bound(self.ctx, int(mode)), "bt_set_step_bound")
 
+    def set_depth_slabs(self, slabs: int) -> None:
+        """1: the reference's single pass; n > 1: frames rendered in n depth
+        slabs, front to back (bt_set_depth_slabs)."""
+        check(self.lib.bt_set_depth_slabs(self.ctx, int(slabs)), "bt_set_depth_slabs")
+
     def compute_normals_rows(self, cam: bt_camera, tile0: int, tile1: int, mode: int = 0, exact: bool = True) -> None:
         """Normals of the tile rows covering [tile0, tile1) only (a sharded
         rank; into the root's planes when a G-buffer is imported)."""
