@@ -27,7 +27,7 @@ REF      ?= /root/reference/proj
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -warn-spills
 CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Iinclude -I$(JSON_DIR) -Wall -Wextra -Wno-unused-parameter -Wno-unknown-pragmas
 
-CU_SRCS  := $(CSRC)/capi.cu $(CSRC)/k_frame.cu $(CSRC)/k_tile.cu $(CSRC)/k_views.cu $(CSRC)/k_tree.cu $(CSRC)/k_trace.cu $(CSRC)/k_util.cu
+CU_SRCS  := $(CSRC)/capi.cu $(CSRC)/k_frame.cu $(CSRC)/k_tile.cu $(CSRC)/k_views.cu $(CSRC)/k_tree.cu $(CSRC)/k_compile.cu $(CSRC)/k_trace.cu $(CSRC)/k_util.cu
 CPP_SRCS := $(wildcard $(CSRC)/host/*.cpp)
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(CSRC)/host/%.cpp,$(OBJ)/host/%.o,$(CPP_SRCS))

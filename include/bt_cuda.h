@@ -174,6 +174,33 @@ BT_API int bt_params_update_device(bt_ctx* ctx, const uint32_t* d_words, const f
                                    const uint32_t* d_counts, uint32_t n, uint32_t stride);
 BT_API int bt_tree_download(bt_ctx* ctx, float* data, uint32_t nwords);
 
+/* GPU compile (replaces blobtree::compile, linear_tree.cpp:70-148, when the
+ * tree STRUCTURE changes per frame).  The scene graph
+ * is a flat node array in any order: operators name their children by index
+ * (left, right), primitives have -1; `root` indexes the root.  Parameters as
+ * in the tree words: primitive translate xyz, rotation wxyz, shape (1-10
+ * floats); operator blend, range (smooth / compact kinds).  The context's
+ * tree becomes the post-order compile of the graph -- words, node records
+ * and primitive words bit-identical to the reference's compile of the same
+ * graph -- with every side table built on the device; `onDevice` = 1 when
+ * `nodes` is a device pointer (a graph edited on the GPU), 0 for host memory.
+ * Errors (BT_EINVAL) mirror compile's: an operator without two children, a
+ * graph that is not one tree rooted at `root`, the 23-bit word space, and
+ * validate_primitive / validate_operator on every node. */
+typedef struct bt_scene_node {
+    uint8_t isPrimitive;
+    uint8_t kind;      /* PrimitiveKind 0..5 or OperatorKind 3..11 */
+    uint8_t pad_[2];
+    int32_t left, right;
+    float params[17];
+} bt_scene_node;
+BT_API int bt_tree_compile(bt_ctx* ctx, const bt_scene_node* nodes, uint32_t n, uint32_t root, int onDevice);
+/* sizes of the context's tree, and its node records / primitive words
+ * (LinearTree::nodes / primitiveWords) */
+BT_API int bt_tree_info(bt_ctx* ctx, uint32_t* nwords, uint32_t* nnodes, uint32_t* nprims);
+BT_API int bt_tree_nodes_download(bt_ctx* ctx, bt_node* nodes, uint32_t nnodes, uint32_t* primWords,
+                                  uint32_t nprims);
+
 /* ---- (a) ROI / VOI ----------------------------------------------------- */
 /* roi per node ordinal (propagate_roi); out may be NULL (device only). */
 BT_API int bt_roi(bt_ctx* ctx, float* out_roi, uint32_t nnodes);

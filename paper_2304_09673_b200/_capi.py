@@ -82,6 +82,9 @@ PROTOTYPES = {
     "bt_params_update": [vp, vp, vp, vp, u32, u32],
     "bt_params_update_device": [vp, vp, vp, vp, u32, u32],
     "bt_tree_download": [vp, vp, u32],
+    "bt_tree_compile": [vp, vp, u32, u32, C.c_int],
+    "bt_tree_info": [vp, vp, vp, vp],
+    "bt_tree_nodes_download": [vp, vp, u32, vp, u32],
     "bt_tree_fast_indices": [vp],
     "bt_roi": [vp, vp, u32],
     "bt_roi_upload": [vp, vp, u32],

@@ -167,6 +167,45 @@ void launch_copy_segments(cudaStream_t st, const void* const* src, void* const* 
 
 // ---- launchers (k_tree.cu) -------------------------------------------
 // compute_fast_indices on the device words (scratch: 4 n int32)
+// ---------------------------------------------------------------- GPU compile (k_compile.cu)
+// bt_scene_node (bt_cuda.h), layout-identical
+struct SceneNodeK {
+    uint8_t isPrimitive, kind, pad_[2];
+    int32_t left, right;
+    float params[17];
+};
+constexpr uint32_t kCmpErrKind = 1, kCmpErrChildren = 2, kCmpErrParents = 3, kCmpErrForest = 4, kCmpErrWords = 5,
+                   kCmpErrParams = 6;
+struct CompileScratch {
+    int32_t* parent;
+    uint8_t* isLeft;
+    int32_t* lm[2];
+    int32_t* next[2];
+    uint4* val[2];
+    uint4* totals;  // (words, nodes, primitives)
+    uint32_t* err;  // smallest (post-order position << 8 | code), or a structure code
+    int2* anc[2];
+    uint32_t *isF, *isU, *fPos, *uPos, *blockSum, *counts;  // counts: frontier, upper entries
+};
+struct CompileNodeRec {  // bt_node (bt_cuda.h), layout-identical
+    uint32_t word, parentWord;
+    int32_t leftChild, rightChild;
+    uint8_t isPrimitive, nodeOp, pad_[2];
+};
+struct CompileOut {
+    float4* words;
+    CompileNodeRec* records;
+    uint32_t *nodeWord, *program, *size, *primWords, *primOrd;
+    int32_t *parentOrd, *compactAnc;
+    uint2* frontier;
+    uint32_t* upper;
+    uint32_t* maxDepth;
+};
+void launch_compile_rank(cudaStream_t st, const SceneNodeK* nodes, uint32_t n, uint32_t root, CompileScratch s);
+void launch_compile_emit(cudaStream_t st, const SceneNodeK* nodes, uint32_t n, CompileScratch s, CompileOut o,
+                         uint32_t frontierCap);
+void launch_compile_chain(cudaStream_t st, const uint32_t* upper, uint32_t m, uint32_t* flags);
+
 void launch_blob_table(cudaStream_t st, const float4* words, const uint32_t* nodeWord, uint32_t n, uint32_t* blobs);
 void launch_fast_indices(cudaStream_t st, float4* words, const uint32_t* nodeWord, const int32_t* parentOrd,
                          uint32_t n, int32_t* scratch);

@@ -112,6 +112,11 @@ struct bt_ctx {
     // (the drop-in free functions upload on every call) only copies the words
     std::vector<bt_node> hostNodes;
     std::vector<uint32_t> hostPrimWords;
+    // GPU compile (bt_tree_compile): the scene graph, scratch, node records
+    DevBuf<SceneNodeK> cmpNodes;
+    DevBuf<uint8_t> cmpScratch;
+    DevBuf<CompileNodeRec> cmpRecords;
+    bool treeFromDevice = false;  // node records live in cmpRecords, not hostNodes
 
     // parameter staging
     DevBuf<uint32_t> pWords, pCounts;
@@ -730,6 +735,9 @@ int bt_ctx_destroy(bt_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->graph) cudaGraphExecDestroy(c->graph);
     c->frontier.release();
+    c->cmpNodes.release();
+    c->cmpScratch.release();
+    c->cmpRecords.release();
     for (auto* b : {&c->primWords, &c->primOrd, &c->nodeWord, &c->fullProgram, &c->upperProgram, &c->blobs, &c->pWords, &c->pCounts,
                     &c->tileCount, &c->tileCursor, &c->tileLocal, &c->blockSum, &c->blockPrefix, &c->offsets,
                     &c->counters, &c->evalCount, &c->tileMaxOverlap, &c->tileCacheBytes, &c->fallback})
@@ -833,7 +841,8 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     c->haveAbuffer = false;
     c->haveGbuffer = false;
     c->viewsFrame = false;
-    if (c->haveTree && nwords == c->nwords && nnodes == c->nnodes && nprims == c->nprims &&
+    if (c->haveTree && !c->treeFromDevice && nwords == c->nwords && nnodes == c->nnodes && nprims == c->nprims &&
+        c->hostNodes.size() == nnodes && c->hostPrimWords.size() == nprims &&
         std::memcmp(c->hostNodes.data(), nodes, (size_t)nnodes * sizeof(bt_node)) == 0 &&
         std::memcmp(c->hostPrimWords.data(), primitiveWords, (size_t)nprims * 4) == 0) {
         // same structure: the side tables stay valid, only parameters changed
@@ -987,9 +996,175 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     c->gradWarps = 0;  // re-sized for the new primitive count on first use
     c->hostNodes.assign(nodes, nodes + nnodes);
     c->hostPrimWords.assign(primitiveWords, primitiveWords + nprims);
+    c->treeFromDevice = false;
     c->haveTree = true;
     c->haveRoi = false;
     c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_tree_compile(bt_ctx* c, const bt_scene_node* nodes, uint32_t n, uint32_t root, int onDevice) {
+    DevGuard dg_(c);
+    static_assert(sizeof(bt_scene_node) == sizeof(SceneNodeK), "bt_scene_node layout");
+    static_assert(sizeof(bt_node) == sizeof(CompileNodeRec), "bt_node layout");
+    if (!c || !nodes) return fail(BT_EINVAL, "null scene graph");
+    if (n == 0) return fail(BT_EINVAL, "empty scene graph");
+    if (root >= n) return fail(BT_EINVAL, "root index out of range");
+    if (n >= BT_ANCESTOR_SENTINEL) return fail(BT_EINVAL, "tree exceeds the 23-bit node index space");
+    c->haveAbuffer = false;
+    c->haveGbuffer = false;
+    c->viewsFrame = false;
+    const SceneNodeK* dn = reinterpret_cast<const SceneNodeK*>(nodes);
+    if (!onDevice) {
+        BT_CUDA(c->cmpNodes.reserve(n));
+        BT_CUDA(cudaMemcpyAsync(c->cmpNodes.ptr, nodes, (size_t)n * sizeof(SceneNodeK), cudaMemcpyHostToDevice,
+                                c->stream));
+        dn = c->cmpNodes.ptr;
+    }
+    // scratch, carved 16-byte aligned
+    const size_t nb = (n + 1023) / 1024 + 1;
+    size_t off = 0;
+    auto carve = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 15) & ~(size_t)15;
+        return o;
+    };
+    const size_t oParent = carve(4 * (size_t)n), oLeft = carve(n), oLm0 = carve(4 * (size_t)n),
+                 oLm1 = carve(4 * (size_t)n), oNx0 = carve(4 * (size_t)n), oNx1 = carve(4 * (size_t)n),
+                 oV0 = carve(16 * (size_t)n), oV1 = carve(16 * (size_t)n), oTot = carve(16), oErr = carve(16),
+                 oA0 = carve(8 * (size_t)n), oA1 = carve(8 * (size_t)n), oF = carve(4 * (size_t)n),
+                 oU = carve(4 * (size_t)n), oFP = carve(4 * (size_t)n), oUP = carve(4 * (size_t)n),
+                 oBS = carve(4 * nb), oCnt = carve(16), oSize = carve(4 * (size_t)n), oDepth = carve(16),
+                 oFlags = carve(16);
+    BT_CUDA(c->cmpScratch.reserve(off));
+    uint8_t* b = c->cmpScratch.ptr;
+    CompileScratch sc;
+    sc.parent = reinterpret_cast<int32_t*>(b + oParent);
+    sc.isLeft = b + oLeft;
+    sc.lm[0] = reinterpret_cast<int32_t*>(b + oLm0);
+    sc.lm[1] = reinterpret_cast<int32_t*>(b + oLm1);
+    sc.next[0] = reinterpret_cast<int32_t*>(b + oNx0);
+    sc.next[1] = reinterpret_cast<int32_t*>(b + oNx1);
+    sc.val[0] = reinterpret_cast<uint4*>(b + oV0);
+    sc.val[1] = reinterpret_cast<uint4*>(b + oV1);
+    sc.totals = reinterpret_cast<uint4*>(b + oTot);
+    sc.err = reinterpret_cast<uint32_t*>(b + oErr);
+    sc.anc[0] = reinterpret_cast<int2*>(b + oA0);
+    sc.anc[1] = reinterpret_cast<int2*>(b + oA1);
+    sc.isF = reinterpret_cast<uint32_t*>(b + oF);
+    sc.isU = reinterpret_cast<uint32_t*>(b + oU);
+    sc.fPos = reinterpret_cast<uint32_t*>(b + oFP);
+    sc.uPos = reinterpret_cast<uint32_t*>(b + oUP);
+    sc.blockSum = reinterpret_cast<uint32_t*>(b + oBS);
+    sc.counts = reinterpret_cast<uint32_t*>(b + oCnt);
+    auto errText = [](uint32_t e) -> std::string {
+        switch (e & 0xFFu) {
+            case kCmpErrKind: return "node kind out of range";
+            case kCmpErrChildren: return "operator node must have two children";
+            case kCmpErrParents: return "scene graph is not a tree (a node has two parents)";
+            case kCmpErrForest: return "scene graph is not one tree rooted at the given root";
+            case kCmpErrWords: return "tree exceeds the 23-bit node index space";
+            default: return "node parameters invalid (node " + std::to_string(e >> 8) + " in post-order)";
+        }
+    };
+    // phase A: structure + list ranking
+    BT_CUDA(cudaMemsetAsync(sc.err, 0xFF, 4, c->stream));
+    launch_compile_rank(c->stream, dn, n, root, sc);
+    uint32_t hdr[8];
+    BT_CUDA(cudaMemcpyAsync(hdr, sc.totals, 32, cudaMemcpyDeviceToHost, c->stream));  // totals + err
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    BT_CUDA(cudaGetLastError());
+    if (hdr[4] != 0xFFFFFFFFu) return fail(BT_EINVAL, errText(hdr[4]));
+    const uint32_t nwords = hdr[0], nprims = hdr[2];
+    // phase B: emit into the tree buffers + side tables
+    c->haveTree = false;
+    BT_CUDA(c->words.reserve(nwords + 8));
+    BT_CUDA(c->primWords.reserve(nprims));
+    BT_CUDA(c->primOrd.reserve(nprims));
+    BT_CUDA(c->nodeWord.reserve(n));
+    BT_CUDA(c->blobs.reserve(nwords));
+    BT_CUDA(c->compactAnc.reserve(n));
+    BT_CUDA(c->parentOrd.reserve(n));
+    BT_CUDA(c->fullProgram.reserve(n));
+    BT_CUDA(c->roi.reserve(n));
+    BT_CUDA(c->frontier.reserve(n));
+    BT_CUDA(c->upperProgram.reserve(n));
+    BT_CUDA(c->vois.reserve(nprims));
+    BT_CUDA(c->cmpRecords.reserve(n));
+    BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
+    BT_CUDA(cudaMemsetAsync(b + oDepth, 0, 16, c->stream));
+    CompileOut o;
+    o.words = c->words.ptr;
+    o.records = c->cmpRecords.ptr;
+    o.nodeWord = c->nodeWord.ptr;
+    o.program = c->fullProgram.ptr;
+    o.size = reinterpret_cast<uint32_t*>(b + oSize);
+    o.primWords = c->primWords.ptr;
+    o.primOrd = c->primOrd.ptr;
+    o.parentOrd = c->parentOrd.ptr;
+    o.compactAnc = c->compactAnc.ptr;
+    o.frontier = c->frontier.ptr;
+    o.upper = c->upperProgram.ptr;
+    o.maxDepth = reinterpret_cast<uint32_t*>(b + oDepth);
+    constexpr uint32_t kCompileFrontierCap = 16;  // any cap gives the same gradient values (capi.cu upload)
+    launch_compile_emit(c->stream, dn, n, sc, o, kCompileFrontierCap);
+    uint32_t tail[4];  // err, nFrontier, nUpper, maxDepth
+    BT_CUDA(cudaMemcpyAsync(&tail[0], sc.err, 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaMemcpyAsync(&tail[1], sc.counts, 8, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaMemcpyAsync(&tail[3], o.maxDepth, 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    BT_CUDA(cudaGetLastError());
+    if (tail[0] != 0xFFFFFFFFu) return fail(BT_EINVAL, errText(tail[0]));
+    uint32_t* flags = reinterpret_cast<uint32_t*>(b + oFlags);
+    launch_compile_chain(c->stream, c->upperProgram.ptr, tail[2], flags);
+    launch_blob_table(c->stream, c->words.ptr, c->nodeWord.ptr, n, c->blobs.ptr);
+    uint32_t fl[2];
+    BT_CUDA(cudaMemcpyAsync(fl, flags, 8, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
+    BT_CUDA(cudaGetLastError());
+    c->nwords = nwords;
+    c->nnodes = n;
+    c->nprims = nprims;
+    c->nvoi = 0;
+    c->fullDepth = tail[3];
+    c->nFrontier = tail[1];
+    c->nUpper = tail[2];
+    c->upperIsChain = (tail[2] && fl[0]) ? 1u : 0u;
+    c->upperIsMinChain = (tail[2] && fl[1]) ? 1u : 0u;
+    c->haveAncLists = false;  // k_roi_all walks the compact-ancestor chain
+    c->gradWarps = 0;
+    c->hostNodes.clear();
+    c->hostPrimWords.clear();
+    c->treeFromDevice = true;
+    c->haveTree = true;
+    c->haveRoi = false;
+    c->bufEpoch++;
+    return BT_OK;
+}
+
+int bt_tree_info(bt_ctx* c, uint32_t* nwords, uint32_t* nnodes, uint32_t* nprims) {
+    DevGuard dg_(c);
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (nwords) *nwords = c->nwords;
+    if (nnodes) *nnodes = c->nnodes;
+    if (nprims) *nprims = c->nprims;
+    return BT_OK;
+}
+
+int bt_tree_nodes_download(bt_ctx* c, bt_node* nodes, uint32_t nnodes, uint32_t* primWords, uint32_t nprims) {
+    DevGuard dg_(c);
+    if (!c || !c->haveTree) return fail(BT_ESTATE, "no tree uploaded");
+    if (nnodes > c->nnodes || nprims > c->nprims) return fail(BT_EINVAL, "count exceeds the tree");
+    if (nodes && nnodes) {
+        if (c->treeFromDevice)
+            BT_CUDA(cudaMemcpyAsync(nodes, c->cmpRecords.ptr, (size_t)nnodes * sizeof(bt_node), cudaMemcpyDeviceToHost,
+                                    c->stream));
+        else
+            std::memcpy(nodes, c->hostNodes.data(), (size_t)nnodes * sizeof(bt_node));
+    }
+    if (primWords && nprims)
+        BT_CUDA(cudaMemcpyAsync(primWords, c->primWords.ptr, (size_t)nprims * 4, cudaMemcpyDeviceToHost, c->stream));
+    BT_CUDA(cudaStreamSynchronize(c->stream));
     return BT_OK;
 }
 

@@ -56,6 +56,10 @@ NODE_DTYPE = np.dtype([("word", "<u4"), ("parentWord", "<u4"), ("leftChild", "<i
 VOI_DTYPE = np.dtype([("family", "u1"), ("pad", "u1", 3), ("primitiveWord", "<u4"), ("center", "<f4", 3),
                       ("radius", "<f4"), ("halfExtents", "<f4", 3), ("rotation", "<f4", 4), ("axisEnd", "<f4", 3)])
 FRAG_DTYPE = np.dtype([("primitiveWord", "<u4"), ("zEntry", "<f4"), ("zExit", "<f4")])
+# bt_scene_node: one node of a scene graph for the GPU compile (bt_tree_compile)
+GRAPH_DTYPE = np.dtype([("isPrimitive", "u1"), ("kind", "u1"), ("pad", "u1", 2), ("left", "<i4"), ("right", "<i4"),
+                        ("params", "<f4", 17)])
+assert GRAPH_DTYPE.itemsize == 80
 assert NODE_DTYPE.itemsize == C.sizeof(bt_node) == 20
 assert VOI_DTYPE.itemsize == C.sizeof(bt_voi) == 64
 assert FRAG_DTYPE.itemsize == C.sizeof(bt_fragment) == 12
@@ -125,6 +129,30 @@ class Scene:
         dc = bt_camera()
         lib.sc_scene_device_camera(h, C.byref(dc))
         return cls(name, seed, h, data, nodes, prims, rw.value, w.value, hh.value, cam, dc)
+
+    def graph(self, seed: int | None = None) -> tuple[np.ndarray, int]:
+        """The scene graph this tree was compiled from (GRAPH_DTYPE), nodes in
+        a random order when `seed` is given; returns (graph, root index)."""
+        n = len(self.nodes)
+        perm = np.arange(n) if seed is None else np.random.default_rng(seed).permutation(n)
+        where = np.empty(n, np.int64)
+        where[perm] = np.arange(n)  # ordinal -> graph index
+        g = np.zeros(n, GRAPH_DTYPE)
+        words = self.data.reshape(-1, 4)
+        for o, rec in enumerate(self.nodes):
+            e = g[where[o]]
+            e["isPrimitive"] = rec["isPrimitive"]
+            e["kind"] = rec["nodeOp"]
+            if rec["isPrimitive"]:
+                cnt = 7 + (1, 3, 2, 3, 3, 10)[rec["nodeOp"]]  # transform + shape floats
+                e["left"] = e["right"] = -1
+                e["params"][:cnt] = words[rec["word"] + 1:].reshape(-1)[:cnt]
+            else:
+                e["left"] = where[rec["leftChild"]]
+                e["right"] = where[rec["rightChild"]]
+                if rec["nodeOp"] > 5:
+                    e["params"][:2] = words[rec["word"] + 1][:2]
+        return g, int(where[n - 1])
 
     @property
     def tiles(self) -> tuple[int, int]:
@@ -224,6 +252,33 @@ class Renderer:
         check(self.lib.bt_tree_upload(self.ctx, ptr(scene.data), len(scene.data) // 4, ptr(scene.nodes),
                                       len(scene.nodes), ptr(scene.prims), len(scene.prims), scene.root_word),
               "bt_tree_upload")
+
+    def compile_tree(self, graph: np.ndarray, root: int, on_device: bool = False) -> None:
+        """GPU compile of a scene graph (GRAPH_DTYPE, any node order) into the
+        context's tree (bt_tree_compile); `graph` may be a device address
+        (int) with `on_device`."""
+        if on_device:
+            addr, n = graph
+            check(self.lib.bt_tree_compile(self.ctx, C.c_void_p(addr), n, root, 1), "bt_tree_compile")
+        else:
+            g = np.ascontiguousarray(graph, GRAPH_DTYPE)
+            check(self.lib.bt_tree_compile(self.ctx, ptr(g), len(g), root, 0), "bt_tree_compile")
+
+    def fast_indices(self) -> None:
+        """compute_fast_indices on the device (bt_tree_fast_indices)."""
+        check(self.lib.bt_tree_fast_indices(self.ctx), "bt_tree_fast_indices")
+
+    def tree_arrays(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(words float32 [nwords*4], node records, primitive words) of the context's tree."""
+        nw, nn, npr = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        check(self.lib.bt_tree_info(self.ctx, C.byref(nw), C.byref(nn), C.byref(npr)), "bt_tree_info")
+        data = np.zeros(nw.value * 4, np.float32)
+        nodes = np.zeros(nn.value, NODE_DTYPE)
+        prims = np.zeros(npr.value, np.uint32)
+        check(self.lib.bt_tree_download(self.ctx, ptr(data), nw.value), "bt_tree_download")
+        check(self.lib.bt_tree_nodes_download(self.ctx, ptr(nodes), nn.value, ptr(prims), npr.value),
+              "bt_tree_nodes_download")
+        return data, nodes, prims
 
     def update_params(self, words: np.ndarray, params: np.ndarray, counts: np.ndarray) -> None:
         check(self.lib.bt_params_update(self.ctx, ptr(words), ptr(params), ptr(counts), len(words), 17),

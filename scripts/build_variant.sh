@@ -5,7 +5,7 @@ NAME=$1; EXTRA=$2
 OBJ=build/var_$NAME
 mkdir -p $OBJ paper_2304_09673_b200/lib/ab
 NV="nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr $EXTRA"
-for f in capi k_frame k_tile k_views k_tree k_trace k_util; do
+for f in capi k_frame k_tile k_views k_tree k_compile k_trace k_util; do
   $NV -c paper_2304_09673_b200/csrc/$f.cu -o $OBJ/$f.o &
 done
 wait
