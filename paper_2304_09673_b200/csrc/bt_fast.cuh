@@ -247,14 +247,21 @@ BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
 // All 32 lanes must call.
 BT_DEV uint32_t warp_uniform(uint32_t v) { return __reduce_or_sync(0xFFFFFFFFu, v); }
 
-// comb record of primitive j: x = (block float4 index << 5) | kind << 2,
-// y = (operator block float4 index << 4) | operator code (j >= 1).
+// comb record of primitive j: x = block byte offset << 16 | 1 << kind,
+// y = the operator's block byte offset << 16 | 1 << operator code (j >= 1).
+// One shift gives the address; the kind and operator dispatch are bit tests
+// (LOP3 + branch each), which nvcc cannot turn into a jump table -- an
+// equality chain on a small integer becomes a BRX table whose index
+// arithmetic and reconvergence barriers cost more than the tests.
 // (Measured: one switch over (kind, operator class) per primitive instead
-// of the two compare chains -- nvcc lowers it to a compare tree plus jump
-// tables -- makes the C3 march 30 % slower.)
-BT_DEV uint32_t comb_prim_rec(uint32_t hdr) { return (((hdr & 0xFFFFu) >> 4) << 5) | (blob_op(hdr) << 2); }
-BT_DEV uint32_t comb_op_rec(uint32_t hdr) { return (((hdr & 0xFFFFu) >> 4) << 4) | blob_op(hdr); }
-BT_DEV uint32_t comb_rec_kind(uint32_t x) { return (x >> 2) & 7u; }
+// of the two compare chains makes the C3 march 30 % slower.)
+BT_DEV uint32_t comb_rec(uint32_t hdr) { return ((hdr & 0xFFF0u) << 16) | (1u << blob_op(hdr)); }
+BT_DEV const float4* comb_rec_block(const float4* blk, uint32_t x) {
+    return reinterpret_cast<const float4*>(reinterpret_cast<const unsigned char*>(blk) + (x >> 16));
+}
+constexpr uint32_t kRecSphere = 1u << 0, kRecEllipsoid = 1u << 1, kRecTorus = 1u << 2, kRecBox = 1u << 3,
+                   kRecCone = 1u << 4;
+constexpr uint32_t kRecCsgUnion = 1u << 3, kRecCompactUnion = 1u << 9, kRecCompact = 7u << 9;
 
 // One primitive value at one point; `kind` is warp-uniform.  The rigid
 // transform is shared by every rotated kind.
@@ -268,34 +275,32 @@ BT_DEV uint32_t comb_rec_kind(uint32_t x) { return (x >> 2) & 7u; }
 // points and parameters (|.| < 1e18, no overflow) they never produce NaN, and
 // the filter there would cost 1.3 % of the march (measured, alternating A/B).
 // tests/test_gpu_reference_scale.py checks NaN-free FMA frames on every kind.
-BT_DEV float fast_prim(uint32_t kind, const float4* B, F3 p) {
-    if (kind == 0u) return f_sphere(B[0], p);
+BT_DEV float fast_prim(uint32_t x, const float4* B, F3 p) {
+    if (x & kRecSphere) return f_sphere(B[0], p);
     const F3 l = f_affine(B[0], B[1], B[2], p);
     const float4 e = B[3];
-    if (kind == 3u) return f_box(e, l);
-    if (kind == 1u) return nan_to_zero(f_ellipsoid(e, B[4], l));
-    if (kind == 2u) return f_torus(e, l);
-    if (kind == 4u) return nan_to_zero(f_cone(e, B[4], l));
+    if (x & kRecBox) return f_box(e, l);
+    if (x & kRecTorus) return f_torus(e, l);
+    if (x & kRecEllipsoid) return nan_to_zero(f_ellipsoid(e, B[4], l));
+    if (x & kRecCone) return nan_to_zero(f_cone(e, B[4], l));
     return f_quadric(e, B[4], B[5], l);
 }
 
 // operator of a comb step: compact and sharp unions first (the blobtree
 // generators' joins), the general chain otherwise
-BT_DEV float comb_op(uint32_t code, const float4* B, float f0, float f1) {
-    if (code == 9u) return fast_compact(0u, B, f0, f1);
-    if (code == 3u) return fminf(f0, f1);
-    return fast_operator(code, B, f0, f1);
+BT_DEV float comb_op(uint32_t y, const float4* B, float f0, float f1) {
+    if (y & kRecCompactUnion) return fast_compact(0u, B, f0, f1);
+    if (y & kRecCsgUnion) return fminf(f0, f1);
+    return fast_operator(31u - __clz(y & 0xFFFFu), B, f0, f1);
 }
 
 BT_DEV float eval_comb(const uint2* rec, uint32_t nPrims, const float4* blk, F3 p) {
-    uint32_t rx = rec[0].x;
-    float v = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
+    uint2 r = rec[0];
+    float v = fast_prim(r.x, comb_rec_block(blk, r.x), p);
     for (uint32_t j = 1; j < nPrims; ++j) {
-        const uint2 r = rec[j];
-        rx = r.x;
-        const uint32_t ry = r.y;
-        const float w = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
-        v = comb_op(ry & 15u, blk + (ry >> 4), v, w);
+        r = rec[j];
+        const float w = fast_prim(r.x, comb_rec_block(blk, r.x), p);
+        v = comb_op(r.y, comb_rec_block(blk, r.y), v, w);
     }
     return v;
 }
@@ -303,17 +308,15 @@ BT_DEV float eval_comb(const uint2* rec, uint32_t nPrims, const float4* blk, F3 
 // eval_comb plus the CSG margin of its compact operators: min over them of
 // max(f0, f1) - d (> 0: every one is in its CSG branch, field.cpp:431)
 BT_DEV float eval_comb_margin(const uint2* rec, uint32_t nPrims, const float4* blk, F3 p, float& margin) {
-    uint32_t rx = rec[0].x;
-    float v = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
+    uint2 r = rec[0];
+    float v = fast_prim(r.x, comb_rec_block(blk, r.x), p);
     float mg = f_inf();
     for (uint32_t j = 1; j < nPrims; ++j) {
-        const uint2 r = rec[j];
-        rx = r.x;
-        const uint32_t ry = r.y, code = ry & 15u;
-        const float4* Bo = blk + (ry >> 4);
-        const float w = fast_prim(comb_rec_kind(rx), blk + (rx >> 5), p);
-        if (code >= 9u) mg = fminf(mg, fmaxf(v, w) - Bo[0].y);
-        v = comb_op(code, Bo, v, w);
+        r = rec[j];
+        const float4* Bo = comb_rec_block(blk, r.y);
+        const float w = fast_prim(r.x, comb_rec_block(blk, r.x), p);
+        if (r.y & kRecCompact) mg = fminf(mg, fmaxf(v, w) - Bo[0].y);
+        v = comb_op(r.y, Bo, v, w);
     }
     margin = mg;
     return v;

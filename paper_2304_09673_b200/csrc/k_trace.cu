@@ -146,11 +146,12 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
                     }
                 }
                 cursor += __popc(idleMask);
+            } else if (idleMask == kFull) {
+                break;  // queue drained, every lane recorded
             }
-            if (!__any_sync(kFull, march_phase(m) != 0u)) {
-                if (cursor >= nPend) break;
-                continue;
-            }
+            // (a refill whose rays all start empty -- t0 > t1 -- leaves a
+            // step with no active lane: it evaluates for nobody and the next
+            // iteration records them; rare enough not to pay a second vote)
         }
         ++steps;
 #ifdef BT_STEP_HIST
@@ -162,7 +163,7 @@ __device__ __forceinline__ void march_interval(const DevTree& t, const Cam& cam,
         const F3 p = ray_point<O>(cam.pos, dir, m.evalT);
         float v;
         float margin = 0.0f;
-        if constexpr (Cls == kClsSingle) v = fast_prim(comb_rec_kind(uaux), s.blocks + (uaux >> 5), p);
+        if constexpr (Cls == kClsSingle) v = fast_prim(uaux, comb_rec_block(s.blocks, uaux), p);
         else if constexpr (Cls == kClsComb) v = eval_comb(s.rec, uaux, s.blocks, p);
         else if constexpr (Cls == kClsCombLip) v = eval_comb_margin(s.rec, uaux, s.blocks, p, margin);
         else if constexpr (Cls == kClsGeneral) eval_view_fast<1>(s.hdr, nView, s.blocks, &p, &v);
@@ -267,8 +268,8 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
                     // left comb: node 0 and every odd node a primitive, every even node > 0 an operator
                     const bool pr = blob_is_prim(nd.x);
                     notComb |= i == 0u ? !pr : pr != ((i & 1u) != 0u);
-                    if (pr) s.rec[(i + 1u) >> 1].x = comb_prim_rec(nd.x);
-                    else s.rec[i >> 1].y = comb_op_rec(nd.x);
+                    if (pr) s.rec[(i + 1u) >> 1].x = comb_rec(nd.x);
+                    else s.rec[i >> 1].y = comb_rec(nd.x);
                 } else {
                     s.word[i] = nd.y;
                 }

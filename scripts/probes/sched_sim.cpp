@@ -1,0 +1,175 @@
+// sched_sim.cpp -- lockstep-step counts of march schedules, from the
+// UNMODIFIED reference's render loop (tracer.cpp:141-236) replayed on one
+// thread with per-(interval, ray) evaluation counts.  Compares:
+//   tile     one warp walks a tile's intervals, 32 lanes over a FIFO ray queue
+//            (what k_march does);
+//   lpt      the same with each interval's rays ordered longest first (an
+//            upper bound: it needs the costs before marching);
+//   pair     horizontally adjacent tiles (2i, 2i+1) walked by one warp; an
+//            interval of each whose pruned views are identical (same active
+//            words) is marched as ONE queue of both tiles' pending rays.
+//   make -C oracle ref && g++ -std=c++20 -O2 -Dblobtree=blobtree_ref -I/root/reference/proj/include \
+//     -I<json> scripts/probes/sched_sim.cpp paper_2304_09673_b200/csrc/scenes/scenes.cpp \
+//     oracle/_ref/libblobtree_ref.a -o /tmp/sched_sim && /tmp/sched_sim C3
+#include <algorithm>
+#include <cstdio>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "blobtree/abuffer.hpp"
+#include "blobtree/tracer.hpp"
+#include "blobtree/traversal.hpp"
+#include "../../paper_2304_09673_b200/csrc/scenes/scenes.hpp"
+
+using namespace blobtree;
+
+struct Iv {
+    std::vector<uint32_t> key;   // active words (the view is a function of them)
+    std::vector<uint32_t> cost;  // evals of each ray marched in this interval (ray order)
+    std::vector<uint32_t> pred;  // predictor: active volumes the ray's interval segment intersects
+};
+
+static uint64_t makespan_pred(const Iv& iv) {
+    std::vector<size_t> idx(iv.cost.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return iv.pred[a] > iv.pred[b]; });
+    std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> h;
+    for (int i = 0; i < 32; ++i) h.push(0);
+    uint64_t m = 0;
+    for (size_t i : idx) {
+        uint64_t t = h.top();
+        h.pop();
+        t += std::max<uint32_t>(iv.cost[i], 1u);
+        m = std::max(m, t);
+        h.push(t);
+    }
+    return m;
+}
+
+static uint64_t makespan(std::vector<uint32_t> c, bool lpt) {
+    if (c.empty()) return 0;
+    if (lpt) std::sort(c.rbegin(), c.rend());
+    std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> h;
+    for (int i = 0; i < 32; ++i) h.push(0);
+    uint64_t m = 0;
+    for (uint32_t x : c) {
+        uint64_t t = h.top();
+        h.pop();
+        // a ray with 0 evals (empty interval) still takes its lane for a step in k_march
+        t += std::max<uint32_t>(x, 1u);
+        m = std::max(m, t);
+        h.push(t);
+    }
+    return m;
+}
+
+int main(int argc, char** argv) {
+    const std::string name = argc > 1 ? argv[1] : "C3";
+    auto sc = scenes::build(name, 0, 0, 0);
+    const LinearTree& tree = sc->tree;
+    RenderConfig cfg;
+    CameraFrame frame(sc->camera);
+    auto roi = propagate_roi(tree);
+    auto vois = build_volumes_of_interest(tree, roi, cfg.hitEpsilon);
+    TileABuffer ab = rasterize_volumes(vois, frame);
+    const int tilesX = frame.tiles_x(), tilesY = frame.tiles_y();
+    std::vector<std::vector<Iv>> tiles(tilesX * tilesY);
+    uint64_t evalsTotal = 0;
+    for (int ty = 0; ty < tilesY; ++ty)
+        for (int tx = 0; tx < tilesX; ++tx) {
+            const auto& frags = ab.at(tx, ty);
+            if (frags.empty()) continue;
+            std::vector<Ray> rays;
+            std::vector<char> found;
+            for (int y = ty * 8; y < std::min((ty + 1) * 8, sc->camera.height); ++y)
+                for (int x = tx * 8; x < std::min((tx + 1) * 8, sc->camera.width); ++x) {
+                    rays.push_back(frame.pixel_ray(x, y));
+                    found.push_back(0);
+                }
+            int remaining = (int)rays.size();
+            TileFetchState fetch;
+            fetch.list = frags;
+            try {
+                while (remaining > 0) {
+                    auto iv = fetch_interval(fetch, frame, cfg);
+                    if (!iv) break;
+                    std::vector<uint32_t> act;
+                    for (const auto& a : fetch.actives) act.push_back(a.word);
+                    PrunedView view = build_pruned_view(tree, act);
+                    if (!view.rootUsed || iv->zEnd <= iv->zBegin) continue;
+                    const float vz0 = frame.view_z_from_ndc(iv->zBegin), vz1 = frame.view_z_from_ndc(iv->zEnd);
+                    Iv rec;
+                    rec.key = act;
+                    for (size_t i = 0; i < rays.size(); ++i) {
+                        if (found[i]) continue;
+                        const Ray& ray = rays[i];
+                        uint32_t evals = 0;
+                        auto fieldAt = [&](float t) { return eval_pruned(view, ray.origin + ray.dir * t); };
+                        TraceResult res =
+                            sphere_trace_interval(fieldAt, ray.t_from_view_z(vz0), ray.t_from_view_z(vz1), cfg, evals);
+                        rec.cost.push_back(evals);
+                        uint32_t np = 0;
+                        const float ta = ray.t_from_view_z(vz0), tb = ray.t_from_view_z(vz1);
+                        for (const auto& a : fetch.actives) {
+                            for (const auto& v : vois)
+                                if (v.primitiveWord == a.word) {
+                                    auto r = ray_volume_intersect(ray, v);
+                                    if (r && r->second >= ta && r->first <= tb) ++np;
+                                    break;
+                                }
+                        }
+                        rec.pred.push_back(np);
+                        evalsTotal += evals;
+                        if (res.hit) {
+                            found[i] = 1;
+                            --remaining;
+                        }
+                    }
+                    tiles[ty * tilesX + tx].push_back(std::move(rec));
+                }
+            } catch (...) {
+            }
+        }
+    uint64_t sTile = 0, sLpt = 0, sPair = 0, ivs = 0, merged = 0, sPred = 0;
+    for (auto& t : tiles)
+        for (auto& iv : t) {
+            sPred += makespan_pred(iv);
+            sTile += makespan(iv.cost, false);
+            sLpt += makespan(iv.cost, true);
+            ++ivs;
+        }
+    // pairs: greedy walk -- merge the heads when their keys match, else march
+    // the head with fewer... (the one of the tile with more intervals left)
+    for (int ty = 0; ty < tilesY; ++ty)
+        for (int tx = 0; tx < tilesX; tx += 2) {
+            auto& A = tiles[ty * tilesX + tx];
+            static std::vector<Iv> empty;
+            auto& B = tx + 1 < tilesX ? tiles[ty * tilesX + tx + 1] : empty;
+            size_t a = 0, b = 0;
+            while (a < A.size() || b < B.size()) {
+                if (a < A.size() && b < B.size() && A[a].key == B[b].key) {
+                    std::vector<uint32_t> c = A[a].cost;
+                    c.insert(c.end(), B[b].cost.begin(), B[b].cost.end());
+                    sPair += makespan(c, false);
+                    ++merged;
+                    ++a;
+                    ++b;
+                } else if (a < A.size() && (b >= B.size() || A.size() - a >= B.size() - b)) {
+                    // look ahead: if B's head matches A's next, march A's head alone
+                    sPair += makespan(A[a].cost, false);
+                    ++a;
+                } else {
+                    sPair += makespan(B[b].cost, false);
+                    ++b;
+                }
+            }
+        }
+    std::printf("%s: evals %llu  intervals %llu  ideal steps %llu\n", name.c_str(), (unsigned long long)evalsTotal,
+                (unsigned long long)ivs, (unsigned long long)((evalsTotal + 31) / 32));
+    std::printf("  tile  %llu steps (util %.3f)\n", (unsigned long long)sTile, evalsTotal / (32.0 * sTile));
+    std::printf("  lpt   %llu steps (util %.3f)\n", (unsigned long long)sLpt, evalsTotal / (32.0 * sLpt));
+    std::printf("  pred  %llu steps (util %.3f)\n", (unsigned long long)sPred, evalsTotal / (32.0 * sPred));
+    std::printf("  pair  %llu steps (util %.3f), %llu merged interval pairs\n", (unsigned long long)sPair,
+                evalsTotal / (32.0 * sPair), (unsigned long long)merged);
+}
