@@ -31,17 +31,21 @@ BT_DEV void affine_rows(const float* P, float4* B) {
 }
 
 // Writes the fast block of one view node (blob may carry a reserved code).
+// Reciprocals and quotients use the approximate MUFU forms (rcp.approx,
+// <= 1 ulp): this is the tolerance path, and IEEE division's slow-path
+// check and call would cost more than the whole conversion.
 BT_DEV void convert_node(uint32_t blob, const float4* raw, float4* B) {
     const uint32_t code = blob_op(blob);
     if (!blob_is_prim(blob)) {
         if (code < 6u || code > 11u) return;  // reserved / sharp: no parameters
         const float4 q = __ldg(raw);
         const float k = q.x, d = q.y;
+        const float invk = FastOps::rcp(k), k6 = k * (1.0f / 6.0f);
         if (code <= 8u) {
-            B[0] = make_float4(k, k / 6.0f, 1.0f / k, 0.0f);
+            B[0] = make_float4(k, k6, invk, 0.0f);
         } else {
-            B[0] = make_float4(k, d, k / 6.0f, 1.0f / k);
-            B[1] = make_float4(6.0f / (6.0f * d - k), 0.0f, 0.0f, 0.0f);
+            B[0] = make_float4(k, d, k6, invk);
+            B[1] = make_float4(FastOps::rcp(d - k6), 0.0f, 0.0f, 0.0f);  // 6 / (6d - k)
         }
         return;
     }
@@ -54,10 +58,12 @@ BT_DEV void convert_node(uint32_t blob, const float4* raw, float4* B) {
     }
     affine_rows(P, B);
     switch (code) {
-        case 1:  // ellipsoid
-            B[3] = make_float4(1.0f / s[0], 1.0f / s[1], 1.0f / s[2], -smin(s[0], smin(s[1], s[2])));
-            B[4] = make_float4(1.0f / (s[0] * s[0]), 1.0f / (s[1] * s[1]), 1.0f / (s[2] * s[2]), 0.0f);
+        case 1: {  // ellipsoid
+            const float i0 = FastOps::rcp(s[0]), i1 = FastOps::rcp(s[1]), i2 = FastOps::rcp(s[2]);
+            B[3] = make_float4(i0, i1, i2, -smin(s[0], smin(s[1], s[2])));
+            B[4] = make_float4(i0 * i0, i1 * i1, i2 * i2, 0.0f);
             break;
+        }
         case 2:  // torus
             B[3] = make_float4(s[0], s[1], 0.0f, 0.0f);
             break;
@@ -65,8 +71,8 @@ BT_DEV void convert_node(uint32_t blob, const float4* raw, float4* B) {
             B[3] = make_float4(s[0], s[1], s[2], 0.0f);
             break;
         case 4: {  // sphere-cone
-            const float b = (s[0] - s[1]) / s[2];
-            const float a = sqrtf(1.0f - b * b);
+            const float b = (s[0] - s[1]) * FastOps::rcp(s[2]);
+            const float a = FastOps::sqrt(1.0f - b * b);
             B[3] = make_float4(s[0], s[1], s[2], b);
             B[4] = make_float4(a, a * s[2], 0.0f, 0.0f);
             break;
@@ -135,8 +141,8 @@ BT_DEV float f_quadric(float4 e, float4 g, float4 h, F3 l) {  // f0 / max(|grad 
 
 // One primitive at NP points; the parameter block is loaded once.
 template <int NP>
-BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v) {
-    if (kind == 0u) {  // sqrt(x) - r of a finite point: never NaN (no filter needed)
+BT_DEV void fast_primitive(uint32_t oh, const float4* B, const F3* p, float* v) {
+    if (oh & 1u) {  // sqrt(x) - r of a finite point: never NaN (no filter needed)
         const float4 c = B[0];
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_sphere(c, p[i]);
@@ -146,17 +152,17 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
     F3 l[NP];
 #pragma unroll
     for (int i = 0; i < NP; ++i) l[i] = f_affine(r0, r1, r2, p[i]);
-    if (kind == 3u) {
+    if (oh & 8u) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_box(e, l[i]);
-    } else if (kind == 2u) {
+    } else if (oh & 4u) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_torus(e, l[i]);
-    } else if (kind == 1u) {
+    } else if (oh & 2u) {
         const float4 f = B[4];
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_ellipsoid(e, f, l[i]);
-    } else if (kind == 4u) {
+    } else if (oh & 16u) {
         const float4 f = B[4];
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = f_cone(e, f, l[i]);
@@ -167,7 +173,7 @@ BT_DEV void fast_primitive(uint32_t kind, const float4* B, const F3* p, float* v
     }
     // the reference's NaN -> 0 filter (field.cpp:283), where a finite point
     // can produce NaN (see fast_prim)
-    if (kind == 1u || kind == 4u) {
+    if (oh & 18u) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) v[i] = nan_to_zero(v[i]);
     }
@@ -206,20 +212,28 @@ BT_DEV float fast_compact(uint32_t fl, const float4* B, float f0, float f1) {
     return fast_smooth(fl, f0, f1, kp * (1.0f / 6.0f), FastOps::rcp(kp));
 }
 
-// compare chain ordered by frequency (sharp and compact unions dominate
-// blobtree views) instead of an indirect jump table
-BT_DEV float fast_operator(uint32_t code, const float4* B, float f0, float f1) {
-    if (code == 9u) return fast_compact(0u, B, f0, f1);
-    if (code == 3u) return fminf(f0, f1);
-    if (code >= 10u) return fast_compact(code - 9u, B, f0, f1);
-    if (code >= 6u) {
+// Operator by its one-hot code (bit `code` of `oh`): bit tests ordered by
+// frequency (compact and sharp unions dominate blobtree views) -- nvcc turns
+// an equality chain on the code into a jump table, which costs more.
+BT_DEV float fast_operator(uint32_t oh, const float4* B, float f0, float f1) {
+    if (oh & (1u << 9)) return fast_compact(0u, B, f0, f1);
+    if (oh & (1u << 3)) return fminf(f0, f1);
+    if (oh & (3u << 10)) return fast_compact((oh & (1u << 10)) ? 1u : 2u, B, f0, f1);
+    if (oh & (7u << 6)) {
         const float4 b0 = B[0];
-        return fast_smooth(code - 6u, f0, f1, b0.y, b0.z);
+        return fast_smooth((oh & (1u << 6)) ? 0u : ((oh & (1u << 7)) ? 1u : 2u), f0, f1, b0.y, b0.z);
     }
-    if (code == 4u) return fmaxf(f0, f1);
-    if (code == 5u) return fmaxf(f0, -f1);
-    return code == 0u ? f_inf() : (code == 1u ? f1 : f0);
+    if (oh & (1u << 4)) return fmaxf(f0, f1);
+    if (oh & (1u << 5)) return fmaxf(f0, -f1);
+    return (oh & 1u) ? f_inf() : ((oh & 2u) ? f1 : f0);
 }
+
+// Header of a staged fast-path node: isPrim(1) | one-hot code (bits 16-27) |
+// block byte offset (16 bits; the fast blocks of a view fit in 5 KB).
+BT_DEV uint32_t fast_hdr(uint32_t hdr) {
+    return (hdr & 0x80000000u) | ((1u << blob_op(hdr)) << 16) | (hdr & 0xFFF0u);
+}
+BT_DEV uint32_t fast_hdr_code(uint32_t fh) { return (fh >> 16) & 0xFFFu; }
 
 // ---------------------------------------------------------------- view classes
 //
@@ -291,7 +305,7 @@ BT_DEV float fast_prim(uint32_t x, const float4* B, F3 p) {
 BT_DEV float comb_op(uint32_t y, const float4* B, float f0, float f1) {
     if (y & kRecCompactUnion) return fast_compact(0u, B, f0, f1);
     if (y & kRecCsgUnion) return fminf(f0, f1);
-    return fast_operator(31u - __clz(y & 0xFFFFu), B, f0, f1);
+    return fast_operator(y & 0xFFFFu, B, f0, f1);
 }
 
 BT_DEV float eval_comb(const uint2* rec, uint32_t nPrims, const float4* blk, F3 p) {
@@ -324,7 +338,8 @@ BT_DEV float eval_comb_margin(const uint2* rec, uint32_t nPrims, const float4* b
 
 constexpr uint32_t kNotAnOp = 0x80000000u;  // a primitive header: ends a fused primitive + operator pair
 
-// Algorithm 3 over the fast blocks of a staged view (`prm` = the blocks in
+// Algorithm 3 over the fast blocks of a staged view (headers in fast_hdr
+// form; `prm` = the blocks in
 // this warp's shared memory), at NP points per lane.  The two top stack
 // entries live in registers (t0 = top, t1 = second): a left comb -- the
 // common blobtree shape -- never touches the local-memory part, deeper
@@ -343,12 +358,12 @@ BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, c
         const uint32_t bn = i + 1 < n ? hdr[i + 1] : kNotAnOp;
         if (blob_is_prim(b)) {
             float v[NP];
-            fast_primitive<NP>(blob_op(b), B, p, v);
+            fast_primitive<NP>(fast_hdr_code(b), B, p, v);
             // a primitive directly followed by an operator (every step of a
             // left comb, the common blobtree shape): combine with the stack top
             // in place, no push / pop
             if (sp >= 1u && !blob_is_prim(bn)) {
-                const uint32_t code = blob_op(bn);
+                const uint32_t code = fast_hdr_code(bn);
                 const float4* Bo = reinterpret_cast<const float4*>(base + (bn & 0xFFFFu));
 #pragma unroll
                 for (int k = 0; k < NP; ++k) t0[k] = fast_operator(code, Bo, t0[k], v[k]);
@@ -367,7 +382,7 @@ BT_DEV void eval_view_fast(const uint32_t* hdr, uint32_t n, const float4* prm, c
             }
             ++sp;
         } else {
-            const uint32_t code = blob_op(b);
+            const uint32_t code = fast_hdr_code(b);
 #pragma unroll
             for (int k = 0; k < NP; ++k) t0[k] = fast_operator(code, B, t1[k], t0[k]);
             --sp;

@@ -258,7 +258,7 @@ __device__ __forceinline__ void march_tile(const DevTree& t, const Cam& cam, con
             bool notComb = false, notLip1 = false, notLipCap = false;
             for (uint32_t i = lane; i < nView; i += 32) {
                 const uint2 nd = vb.nodes[ra.z + i];
-                s.hdr[i] = nd.x;
+                s.hdr[i] = fits ? fast_hdr(nd.x) : nd.x;
                 if (SB) {
                     notLip1 |= !node_is_one_lipschitz(nd.x);
                     notLipCap |= !node_is_lipschitz_capable(nd.x);
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(kGradViewWarps * 32) k_gradient_view(DevTree t
         const bool fits = rec.nBlocks <= kMarchBlocks;
         for (uint32_t j = lane; j < nView; j += 32) {
             const uint2 nd = vb.nodes[rec.nodeOff + j];
-            sh[w][j] = nd.x;
+            sh[w][j] = fits ? fast_hdr(nd.x) : nd.x;
             sw[w][j] = nd.y;
             if (fits) convert_node(nd.x, t.words + nd.y + 1, blk[w] + ((nd.x & 0xFFFFu) >> 4));
         }
