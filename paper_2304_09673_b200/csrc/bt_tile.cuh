@@ -110,14 +110,16 @@ BT_DEV float eval_staged(const uint32_t* hdr, const uint32_t* word, uint32_t n, 
 //
 // State: the accepted sample (t, f), the end t1, the saved sphere
 // (savedT, savedF), the point being evaluated (evalT), and st:
-//   phase 0 done, 1 ACCEPT (f(t0), or a back-off sample: taken as is),
-//         2 MAIN (a step: overshoot-tested while relaxed);
-//   kSaved  a saved sphere is pending -- relaxation is off exactly while one
-//           is (relaxOn == !savedValid is an invariant of the reference loop,
-//           so one flag carries both);
+//   kActive  the ray is marching (phase != 0); with kMain clear the sample
+//            is ACCEPTed as is (f(t0), or a back-off sample), with kMain set
+//            it is a MAIN step (overshoot-tested while relaxed);
+//   kSaved   a saved sphere is pending -- relaxation is off exactly while one
+//            is (relaxOn == !savedValid is an invariant of the reference loop,
+//            so one flag carries both);
+//   kTestOv  kMain and not kSaved: the step is overshoot-tested (kept as its
+//            own bit so the test is one LOP3);
 //   kHitFlag on completion: t holds the hit position.
-constexpr uint32_t kPhaseMask = 3u;
-constexpr uint32_t kSaved = 4u, kHitFlag = 8u;
+constexpr uint32_t kActive = 1u, kMain = 2u, kSaved = 4u, kHitFlag = 8u, kTestOv = 64u;
 // bt_set_step_bound(1), comb views with compact operators: the step from the
 // accepted point t (kLipT) / from the saved sphere (kLipS) was bounded with
 // L = 1 (see march_consume)
@@ -128,7 +130,7 @@ struct March {
     uint32_t st, evals;
 };
 
-BT_DEV uint32_t march_phase(const March& m) { return m.st & kPhaseMask; }
+BT_DEV uint32_t march_phase(const March& m) { return m.st & kActive; }
 BT_DEV bool march_hit(const March& m) { return (m.st & kHitFlag) != 0u; }
 
 BT_DEV void march_idle(March& m) {
@@ -142,7 +144,7 @@ BT_DEV void march_begin(March& m, float t0, float t1) {
     m.t1 = t1;
     m.t = 0.0f;
     m.evalT = t0;
-    m.st = t0 > t1 ? 0u : 1u;  // t0 > t1: an empty interval, a miss without evaluation
+    m.st = t0 > t1 ? 0u : kActive;  // ACCEPT f(t0); t0 > t1: an empty interval, a miss without evaluation
 }
 
 // One field value v = f(evalT) consumed.  The reference loop, per sample:
@@ -179,12 +181,12 @@ BT_DEV void march_consume(March& m, float v, const TraceParams& tp, bool lip1 = 
     // the march before the step is used.
     m.evals++;
     const float tn = m.evalT;
-    const bool mainStep = (m.st & 2u) != 0u;
+    const bool testOv = (m.st & kTestOv) != 0u;
     const bool sv = (m.st & kSaved) != 0u;
     const float sT = m.savedT, sF = m.savedF;
     const float Lt = Lip && (m.st & kLipT) ? 1.0f : tp.L, invLt = Lip && (m.st & kLipT) ? 1.0f : tp.invL;
     const float invLn = Lip && lip1 ? 1.0f : tp.invL, invLs = Lip && (m.st & kLipS) ? 1.0f : tp.invL;
-    const bool ovT = mainStep & !sv &
+    const bool ovT = testOv &
                      ((E::mul(E::sub(tn, m.t), Lt) >= E::add(m.f, fabsf(v))) | (v < -tp.hitEps));
     const float tb = E::add(m.t, fmaxf(E::mul(m.f, invLt), tp.minStep));
     const bool ov = ovT & !(tb >= tn);
@@ -210,7 +212,8 @@ BT_DEV void march_consume(March& m, float v, const TraceParams& tp, bool lip1 = 
     m.t = ov ? m.t : T;
     m.f = ov ? m.f : (reuse ? sF : v);
     m.evalT = ov ? tb : (beyond ? m.t1 : En);
-    uint32_t next = ((ov | (sv & !reach)) ? kSaved : 0u) | (ov ? 1u : 2u);
+    const bool keepSaved = sv & !reach;
+    uint32_t next = ov ? (kActive | kSaved) : (keepSaved ? (kActive | kMain | kSaved) : (kActive | kMain | kTestOv));
     if (Lip) {
         const uint32_t lipT = ov ? (m.st & kLipT) : ((reuse ? (m.st & kLipS) != 0u : lip1) ? kLipT : 0u);
         const uint32_t lipS = ov ? (lip1 ? kLipS : 0u) : ((sv & !reach) ? (m.st & kLipS) : 0u);
