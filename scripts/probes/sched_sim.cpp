@@ -28,7 +28,37 @@ struct Iv {
     std::vector<uint32_t> key;   // active words (the view is a function of them)
     std::vector<uint32_t> cost;  // evals of each ray marched in this interval (ray order)
     std::vector<uint32_t> pred;  // predictor: active volumes the ray's interval segment intersects
+    std::vector<uint32_t> ray;   // ray index (in the tile) of each cost entry
 };
+
+// queue order by a per-ray key, longest first; `buckets` > 0: only the class
+// of the key relative to the tile's maximum (>= max/2, >= max/4, ...) counts
+static uint64_t makespan_key(const Iv& iv, const std::vector<uint32_t>& key, int buckets) {
+    std::vector<size_t> idx(iv.cost.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    uint32_t mx = 1;
+    for (uint32_t k : key) mx = std::max(mx, k);
+    auto cls = [&](size_t i) -> int64_t {
+        const uint32_t k = key[iv.ray[i]];
+        if (buckets <= 0) return k;
+        int c = 0;
+        for (int b = 1; b < buckets; ++b)
+            if ((uint64_t)k << b >= mx) { c = buckets - b; break; }
+        return c;
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return cls(a) > cls(b); });
+    std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> h;
+    for (int i = 0; i < 32; ++i) h.push(0);
+    uint64_t m = 0;
+    for (size_t i : idx) {
+        uint64_t t = h.top();
+        h.pop();
+        t += std::max<uint32_t>(iv.cost[i], 1u);
+        m = std::max(m, t);
+        h.push(t);
+    }
+    return m;
+}
 
 static uint64_t makespan_pred(const Iv& iv) {
     std::vector<size_t> idx(iv.cost.size());
@@ -109,6 +139,7 @@ int main(int argc, char** argv) {
                         TraceResult res =
                             sphere_trace_interval(fieldAt, ray.t_from_view_z(vz0), ray.t_from_view_z(vz1), cfg, evals);
                         rec.cost.push_back(evals);
+                        rec.ray.push_back((uint32_t)i);
                         uint32_t np = 0;
                         const float ta = ray.t_from_view_z(vz0), tb = ray.t_from_view_z(vz1);
                         for (const auto& a : fetch.actives) {
@@ -131,7 +162,22 @@ int main(int argc, char** argv) {
             } catch (...) {
             }
         }
-    uint64_t sTile = 0, sLpt = 0, sPair = 0, ivs = 0, merged = 0, sPred = 0;
+    uint64_t sTile = 0, sLpt = 0, sPair = 0, ivs = 0, merged = 0, sPred = 0, sTot = 0, sB2 = 0, sB4 = 0, sSoFar = 0;
+    for (auto& t : tiles) {
+        std::vector<uint32_t> tot(64, 0);
+        for (auto& iv : t)
+            for (size_t i = 0; i < iv.cost.size(); ++i) tot[iv.ray[i]] += iv.cost[i];
+        std::vector<uint32_t> sofar(64, 0);
+        for (auto& iv : t) {
+            sSoFar += makespan_key(iv, sofar, 0);
+            for (size_t i = 0; i < iv.cost.size(); ++i) sofar[iv.ray[i]] += iv.cost[i];
+        }
+        for (auto& iv : t) {
+            sTot += makespan_key(iv, tot, 0);
+            sB2 += makespan_key(iv, tot, 2);
+            sB4 += makespan_key(iv, tot, 4);
+        }
+    }
     for (auto& t : tiles)
         for (auto& iv : t) {
             sPred += makespan_pred(iv);
@@ -169,6 +215,9 @@ int main(int argc, char** argv) {
                 (unsigned long long)ivs, (unsigned long long)((evalsTotal + 31) / 32));
     std::printf("  tile  %llu steps (util %.3f)\n", (unsigned long long)sTile, evalsTotal / (32.0 * sTile));
     std::printf("  lpt   %llu steps (util %.3f)\n", (unsigned long long)sLpt, evalsTotal / (32.0 * sLpt));
+    std::printf("  total-key lpt %llu  2-class %llu  4-class %llu\n", (unsigned long long)sTot, (unsigned long long)sB2,
+                (unsigned long long)sB4);
+    std::printf("  so-far-key lpt %llu\n", (unsigned long long)sSoFar);
     std::printf("  pred  %llu steps (util %.3f)\n", (unsigned long long)sPred, evalsTotal / (32.0 * sPred));
     std::printf("  pair  %llu steps (util %.3f), %llu merged interval pairs\n", (unsigned long long)sPair,
                 evalsTotal / (32.0 * sPair), (unsigned long long)merged);
