@@ -105,6 +105,7 @@ struct bt_ctx {
     bool haveAncLists = false;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
+    DevBuf<RasterVol> rasterVols;  // [nvoi] the volumes' ray-test terms for the frame's camera (k_pairs)
     uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
     bool haveTree = false;
     bool haveRoi = false;
@@ -258,6 +259,7 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.sbBlockSum = c->sbBlockSum.ptr;
     f.sbBlockPrefix = c->sbBlockPrefix.ptr;
     f.sbList = c->sbList.ptr;
+    f.rasterVols = c->rasterVols.ptr;
     f.tileFrag = c->tileFrag.ptr;
     f.pairCap = std::min(c->pairs.cap, c->sbList.cap);
     f.poolCap = c->frags.cap;
@@ -750,6 +752,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->fastScratch.release();
     c->roi.release();
     c->vois.release();
+    c->rasterVols.release();
     c->pParams.release();
     c->rays.release();
     c->cones.release();
@@ -961,6 +964,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(c->frontier.reserve(frontier.size()));
     BT_CUDA(c->upperProgram.reserve(upper.size()));
     BT_CUDA(c->vois.reserve(nprims));
+    BT_CUDA(c->rasterVols.reserve(nprims));
     BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
     BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->primWords.ptr, primitiveWords, nprims * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1090,6 +1094,7 @@ int bt_tree_compile(bt_ctx* c, const bt_scene_node* nodes, uint32_t n, uint32_t 
     BT_CUDA(c->frontier.reserve(n));
     BT_CUDA(c->upperProgram.reserve(n));
     BT_CUDA(c->vois.reserve(nprims));
+    BT_CUDA(c->rasterVols.reserve(nprims));
     BT_CUDA(c->cmpRecords.reserve(n));
     BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
     BT_CUDA(cudaMemsetAsync(b + oDepth, 0, 16, c->stream));
@@ -1292,6 +1297,7 @@ int bt_voi_upload(bt_ctx* c, const bt_voi* v, uint32_t n) {
     }
     if (n > c->vois.cap) {
         BT_CUDA(c->vois.reserve(n));
+        BT_CUDA(c->rasterVols.reserve(n));
         c->bufEpoch++;
     }
     if (n) BT_CUDA(cudaMemcpyAsync(c->vois.ptr, h.data(), n * sizeof(Voi), cudaMemcpyHostToDevice, c->stream));

@@ -63,9 +63,11 @@ struct TileSmem {  // views pass, per warp
 // mapped to NDC once (ndc_from_view_z is monotone: bit for bit the
 // reference's per-ray min / max, two divisions per volume instead of two per ray).
 template <bool Fm>
-__device__ __forceinline__ bool raster_volume(const Cam& cam, const Voi& v, const float4* rays, float& entryOut,
+__device__ __forceinline__ bool raster_volume(const Cam& cam, const RasterVol& rv, const float4* rays, float& entryOut,
                                               float& exitOut) {
-    const RayVolPre pre = ray_vol_pre(v, cam.pos);  // the ray-independent terms, once per volume
+    // the ray-independent terms, once per volume and frame (k_pairs, raster_vol_make)
+    const uint32_t family = raster_vol_family(rv);
+    const F3 a{rv.q0.x, rv.q0.y, rv.q0.z};
     float entry = f_inf(), exitv = -f_inf();
     bool any = false;
 #pragma unroll kRasterUnroll
@@ -75,12 +77,12 @@ __device__ __forceinline__ bool raster_volume(const Cam& cam, const Voi& v, cons
         const F3 d{rd.x, rd.y, rd.z};
         float t0, t1;
         bool hit;
-        if (v.family == 0u)
-            hit = ray_sphere_pre(pre.a, pre.cc, d, t0, t1);
-        else if (v.family == 1u)
-            hit = ray_obb_local<Fm>(pre.a, d, v.rot, v.half, t0, t1);
+        if (family == 0u)
+            hit = ray_sphere_pre(a, rv.q0.w, d, t0, t1);
+        else if (family == 1u)
+            hit = ray_obb_local<Fm>(a, d, Q4{rv.q1.x, rv.q1.y, rv.q1.z, rv.q1.w}, F3{rv.q2.x, rv.q2.y, rv.q2.z}, t0, t1);
         else
-            hit = ray_capsule_pre<Fm>(pre, d, t0, t1);
+            hit = ray_capsule_pre<Fm>(raster_vol_capsule(rv), d, t0, t1);
         if (!hit) continue;
         float vz0 = E::mul(t0, rd.w), vz1 = E::mul(t1, rd.w);
         if (vz1 < cam.nearZ || vz0 > cam.farZ) continue;
@@ -159,10 +161,11 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
         // 2. the survivors' exact ray tests, one volume at a time
         for (uint32_t i = 0; i < cnt; ++i) {
             const uint32_t vk = list[i];
-            const Voi v = vois[vk];
+            const RasterVol rv = fb.rasterVols[vk];
             float en, ex;
-            if (raster_volume<Fm>(cam, v, rays, en, ex)) {
-                if (lane == 0 && nf < sinkCap) sink[nf] = make_uint4(v.word, __float_as_uint(en), __float_as_uint(ex), vk);
+            if (raster_volume<Fm>(cam, rv, rays, en, ex)) {
+                if (lane == 0 && nf < sinkCap)
+                    sink[nf] = make_uint4(raster_vol_word(rv), __float_as_uint(en), __float_as_uint(ex), vk);
                 ++nf;
             }
         }

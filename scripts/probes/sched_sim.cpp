@@ -211,6 +211,39 @@ int main(int argc, char** argv) {
                 }
             }
         }
+    // runs of R horizontally adjacent tiles walked by one warp in waves: wave
+    // k marches interval k of every tile of the run (the ones still having
+    // one); consecutive items of a wave with identical views share one queue
+    for (int R : {2, 4, 8, 16}) {
+        uint64_t steps = 0, items = 0, groups = 0;
+        for (int ty = 0; ty < tilesY; ++ty)
+            for (int tx0 = 0; tx0 < tilesX; tx0 += R) {
+                const int tx1 = std::min(tilesX, tx0 + R);
+                size_t maxK = 0;
+                for (int tx = tx0; tx < tx1; ++tx) maxK = std::max(maxK, tiles[ty * tilesX + tx].size());
+                for (size_t k = 0; k < maxK; ++k) {
+                    std::vector<uint32_t> q;
+                    const std::vector<uint32_t>* key = nullptr;
+                    for (int tx = tx0; tx < tx1; ++tx) {
+                        auto& T = tiles[ty * tilesX + tx];
+                        if (k >= T.size()) continue;
+                        ++items;
+                        if (key && *key == T[k].key) {
+                            q.insert(q.end(), T[k].cost.begin(), T[k].cost.end());
+                        } else {
+                            steps += makespan(q, false);
+                            if (!q.empty()) ++groups;
+                            q = T[k].cost;
+                            key = &T[k].key;
+                        }
+                    }
+                    steps += makespan(q, false);
+                    if (!q.empty()) ++groups;
+                }
+            }
+        std::printf("  run%-2d %llu steps (util %.3f), %llu items in %llu queues\n", R, (unsigned long long)steps,
+                    evalsTotal / (32.0 * steps), (unsigned long long)items, (unsigned long long)groups);
+    }
     std::printf("%s: evals %llu  intervals %llu  ideal steps %llu\n", name.c_str(), (unsigned long long)evalsTotal,
                 (unsigned long long)ivs, (unsigned long long)((evalsTotal + 31) / 32));
     std::printf("  tile  %llu steps (util %.3f)\n", (unsigned long long)sTile, evalsTotal / (32.0 * sTile));
