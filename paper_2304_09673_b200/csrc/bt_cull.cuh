@@ -74,6 +74,67 @@ __device__ __forceinline__ bool volume_pyramid_may_touch(const float4* pl, F3 ap
 }
 
 
+// A volume ready for k_tile_raster's culls, for the frame's camera, built once
+// per frame and volume (k_pairs) instead of once per (tile, candidate):
+//   q0 = (bs.c - apex, |bs.c - apex|^2)   cone_may_touch's ray-independent
+//        terms, exact ops as there (bit-identical cone test); for boxes and
+//        spheres also the pyramid test's centre offset (the same single
+//        rounded subtraction)
+//   q1 = (bs.r, pad, family, support radius)
+//   q2, q3, q4 = box: the half-axis vectors a0, a1, a2; capsule: a0 - apex,
+//        a1 - apex (q4 unused)
+struct CullVol {
+    float4 q0, q1, q2, q3, q4;
+};
+
+__device__ __forceinline__ CullVol cull_vol_make(const Sphere& bs, const VolumeSupport& s, F3 apex) {
+    CullVol r;
+    const F3 cv = vsub<E>(bs.c, apex);
+    r.q0 = make_float4(cv.x, cv.y, cv.z, vdot<E>(cv, cv));
+    r.q1 = make_float4(bs.r, s.pad, __uint_as_float(s.family), s.r);
+    if (s.family == 1u) {
+        r.q2 = make_float4(s.a0.x, s.a0.y, s.a0.z, 0.0f);
+        r.q3 = make_float4(s.a1.x, s.a1.y, s.a1.z, 0.0f);
+        r.q4 = make_float4(s.a2.x, s.a2.y, s.a2.z, 0.0f);
+    } else {
+        r.q2 = make_float4(s.a0.x - apex.x, s.a0.y - apex.y, s.a0.z - apex.z, 0.0f);
+        r.q3 = make_float4(s.a1.x - apex.x, s.a1.y - apex.y, s.a1.z - apex.z, 0.0f);
+        r.q4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+    return r;
+}
+
+// cone_may_touch (the reference's tile cone test, abuffer.cpp:140-149) with
+// the volume's terms precomputed: bit-identical
+__device__ __forceinline__ bool cullvol_cone_may_touch(const Cone& k, const CullVol& r) {
+    const F3 v{r.q0.x, r.q0.y, r.q0.z};
+    const float x = vdot<E>(v, k.axis);
+    const float yy = E::sub(r.q0.w, E::mul(x, x));
+    const float y = E::sqrt(smax(yy, 0.0f));
+    return E::sub(E::mul(k.cosH, y), E::mul(k.sinH, x)) <= r.q1.x;
+}
+
+// volume_pyramid_may_touch with the apex already subtracted
+__device__ __forceinline__ bool cullvol_pyramid_may_touch(const float4* pl, const CullVol& r) {
+    const uint32_t family = __float_as_uint(r.q1.z);
+    const float pad = r.q1.y;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float4 n = pl[e];
+        float reach;
+        if (family == 1u) {
+            reach = n.x * r.q0.x + n.y * r.q0.y + n.z * r.q0.z + fabsf(n.x * r.q2.x + n.y * r.q2.y + n.z * r.q2.z) +
+                    fabsf(n.x * r.q3.x + n.y * r.q3.y + n.z * r.q3.z) + fabsf(n.x * r.q4.x + n.y * r.q4.y + n.z * r.q4.z);
+        } else if (family == 2u) {
+            reach = fmaxf(n.x * r.q2.x + n.y * r.q2.y + n.z * r.q2.z, n.x * r.q3.x + n.y * r.q3.y + n.z * r.q3.z) + r.q1.w;
+        } else {
+            reach = n.x * r.q0.x + n.y * r.q0.y + n.z * r.q0.z + r.q1.w;
+        }
+        if (reach < -pad) return false;
+    }
+    return true;
+}
+
 // key order of insert_sorted (abuffer.cpp:166-173): (zEntry, word); equal
 // keys keep volume order (upper_bound insertion in volume order), hence the
 // volume index tiebreak.  Fragment records: (word, entry bits, exit bits, voi).

@@ -69,6 +69,7 @@ struct FrameBufs {
     uint32_t* sbBlockPrefix = nullptr;
     uint32_t* sbList = nullptr;      // [pairCap] volume indices, superblock-major
     uint2* tileFrag = nullptr;       // [tiles] (first fragment, count) of each tile's sorted list in frags
+    struct CullVol* cullVols = nullptr;  // [volumes] cull terms for the frame's camera (k_pairs -> k_tile_raster)
     RasterVol* rasterVols = nullptr; // [volumes] ray-test terms for the frame's camera (k_pairs -> k_tile_raster)
     uint64_t pairCap = 0, poolCap = 0, fragCap = 0;
 };

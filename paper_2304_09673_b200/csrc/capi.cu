@@ -21,6 +21,7 @@
 
 #include "../../include/bt_cuda.h"
 #include "bt_device.h"
+#include "bt_cull.cuh"
 
 using namespace btk;
 
@@ -105,6 +106,7 @@ struct bt_ctx {
     bool haveAncLists = false;
     DevBuf<float> roi;
     DevBuf<Voi> vois;
+    DevBuf<CullVol> cullVols;      // [nvoi] the volumes' cull terms for the frame's camera (k_pairs)
     DevBuf<RasterVol> rasterVols;  // [nvoi] the volumes' ray-test terms for the frame's camera (k_pairs)
     uint32_t nwords = 0, nnodes = 0, nprims = 0, nvoi = 0, fullDepth = 0;
     bool haveTree = false;
@@ -260,6 +262,7 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.sbBlockPrefix = c->sbBlockPrefix.ptr;
     f.sbList = c->sbList.ptr;
     f.rasterVols = c->rasterVols.ptr;
+    f.cullVols = c->cullVols.ptr;
     f.tileFrag = c->tileFrag.ptr;
     f.pairCap = std::min(c->pairs.cap, c->sbList.cap);
     f.poolCap = c->frags.cap;
@@ -753,6 +756,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->roi.release();
     c->vois.release();
     c->rasterVols.release();
+    c->cullVols.release();
     c->pParams.release();
     c->rays.release();
     c->cones.release();
@@ -965,6 +969,7 @@ int bt_tree_upload(bt_ctx* c, const float* data, uint32_t nwords, const bt_node*
     BT_CUDA(c->upperProgram.reserve(upper.size()));
     BT_CUDA(c->vois.reserve(nprims));
     BT_CUDA(c->rasterVols.reserve(nprims));
+    BT_CUDA(c->cullVols.reserve(nprims));
     BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
     BT_CUDA(cudaMemcpyAsync(c->words.ptr, data, (size_t)nwords * 16, cudaMemcpyHostToDevice, c->stream));
     BT_CUDA(cudaMemcpyAsync(c->primWords.ptr, primitiveWords, nprims * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1095,6 +1100,7 @@ int bt_tree_compile(bt_ctx* c, const bt_scene_node* nodes, uint32_t n, uint32_t 
     BT_CUDA(c->upperProgram.reserve(n));
     BT_CUDA(c->vois.reserve(nprims));
     BT_CUDA(c->rasterVols.reserve(nprims));
+    BT_CUDA(c->cullVols.reserve(nprims));
     BT_CUDA(c->cmpRecords.reserve(n));
     BT_CUDA(cudaMemsetAsync(c->words.ptr, 0, (nwords + 8) * sizeof(float4), c->stream));
     BT_CUDA(cudaMemsetAsync(b + oDepth, 0, 16, c->stream));
@@ -1298,6 +1304,7 @@ int bt_voi_upload(bt_ctx* c, const bt_voi* v, uint32_t n) {
     if (n > c->vois.cap) {
         BT_CUDA(c->vois.reserve(n));
         BT_CUDA(c->rasterVols.reserve(n));
+        BT_CUDA(c->cullVols.reserve(n));
         c->bufEpoch++;
     }
     if (n) BT_CUDA(cudaMemcpyAsync(c->vois.ptr, h.data(), n * sizeof(Voi), cudaMemcpyHostToDevice, c->stream));

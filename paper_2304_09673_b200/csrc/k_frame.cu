@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
     const VolumeSupport sup = volume_support(v, cam.pos);
     const int sbX = (tilesX + kSB - 1) / kSB;
     // the volume's ray-test terms for this camera, once per frame (k_tile_raster)
-    if (blockIdx.y == 0 && lane == 0) fb.rasterVols[warp] = raster_vol_make(v, cam.pos);
+    if (blockIdx.y == 0 && lane == 0) {
+        fb.rasterVols[warp] = raster_vol_make(v, cam.pos);
+        fb.cullVols[warp] = cull_vol_make(bs, sup, cam.pos);
+    }
     int rx0, rx1, ry0, ry1;
     sphere_sb_rect(cam, bs, tilesX, tilesY, rx0, rx1, ry0, ry1);
     // ... within the superblock rows [sbLo, sbHi) that meet [tile0, tile1)

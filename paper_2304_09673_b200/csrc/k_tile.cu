@@ -146,9 +146,8 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
             bool pass = false;
             if (j < nCand) {
                 vi = cand[j];
-                const Voi v = vois[vi];
-                pass = cone_may_touch(cone, cam.pos, bounding_sphere(v)) &&
-                       volume_pyramid_may_touch(pyramid, cam.pos, volume_support(v, cam.pos));
+                const CullVol cv = fb.cullVols[vi];
+                pass = cullvol_cone_may_touch(cone, cv) && cullvol_pyramid_may_touch(pyramid, cv);
             }
             const uint32_t m = __ballot_sync(kFull, pass);
             if (pass) list[cnt + __popc(m & ((1u << lane) - 1u))] = vi;
