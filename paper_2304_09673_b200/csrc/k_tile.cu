@@ -110,8 +110,8 @@ constexpr uint32_t kCullList = 128;  // survivors of the tile cull kept per warp
 
 template <bool Fm>
 __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs& fb, uint32_t tile, int tx, int ty,
-                                int tilesX, uint32_t* list, float4* rays, uint4* sink, uint32_t sinkCap,
-                                uint32_t& tested) {
+                                int tilesX, uint32_t* list, RasterVol* vstage, float4* rays, uint4* sink,
+                                uint32_t sinkCap, uint32_t& tested) {
     const uint32_t lane = threadIdx.x & 31u;
     // the tile's 64 rays, staged once for all its volumes (dot(dir, forward)
     // > 0 inside the image; 0 marks pixels outside it)
@@ -157,18 +157,26 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
         }
         tested += cnt;
         __syncwarp();
-        // 2. the survivors' exact ray tests, one volume at a time
-        for (uint32_t i = 0; i < cnt; ++i) {
-            const uint32_t vk = list[i];
-            const RasterVol rv = fb.rasterVols[vk];
-            float en, ex;
-            if (raster_volume<Fm>(cam, rv, rays, en, ex)) {
-                if (lane == 0 && nf < sinkCap)
-                    sink[nf] = make_uint4(raster_vol_word(rv), __float_as_uint(en), __float_as_uint(ex), vk);
-                ++nf;
+        // 2. the survivors' exact ray tests, one volume at a time; the
+        // volumes' records are gathered 32 at a time into shared memory (one
+        // load per lane, all in flight together) instead of one dependent
+        // load per volume
+        for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+            const uint32_t nc = min(32u, cnt - c0);
+            if (lane < nc) vstage[lane] = fb.rasterVols[list[c0 + lane]];
+            __syncwarp();
+            for (uint32_t i = 0; i < nc; ++i) {
+                const RasterVol rv = vstage[i];
+                float en, ex;
+                if (raster_volume<Fm>(cam, rv, rays, en, ex)) {
+                    if (lane == 0 && nf < sinkCap)
+                        sink[nf] = make_uint4(raster_vol_word(rv), __float_as_uint(en), __float_as_uint(ex),
+                                              list[c0 + i]);
+                    ++nf;
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     return nf;
 }
@@ -474,6 +482,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
     k_tile_raster(Cam cam, const Voi* vois, FrameBufs fb, int tilesX, uint32_t tile0, uint32_t tile1) {
     __shared__ uint4 stage[kTileWarps][kTileStage];
     __shared__ uint32_t culled[kTileWarps][kCullList];
+    __shared__ RasterVol vstaged[kTileWarps][32];
     __shared__ float4 tileRays[kTileWarps][64];
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     // a (volume, superblock) pair list that outgrew its buffer: empty,
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
         uint32_t fbase = 0, nf = 0;
         if (!pairsLost) {
             uint32_t tested = 0;
-            nf = raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], stage[wid], kTileStage, tested);
+            nf = raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], vstaged[wid], tileRays[wid], stage[wid], kTileStage, tested);
             testedSum += tested;
         }
         if (lane == 0 && nf) fbase = atomicAdd(&fb.counters[kCntFrags], nf);
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
             nf = 0;
         } else if (nf > kTileStage) {  // rare: too many fragments to sort in shared memory
             uint32_t tested = 0;
-            raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], tileRays[wid], fb.unsorted + fbase, nf, tested);
+            raster_tile<Fm>(cam, vois, fb, tile, tx, ty, tilesX, culled[wid], vstaged[wid], tileRays[wid], fb.unsorted + fbase, nf, tested);
             __syncwarp();
             sort_tile(fb.unsorted + fbase, nf, fb.frags + fbase);
         } else if (nf) {
