@@ -244,6 +244,27 @@ int main(int argc, char** argv) {
         std::printf("  run%-2d %llu steps (util %.3f), %llu items in %llu queues\n", R, (unsigned long long)steps,
                     evalsTotal / (32.0 * steps), (unsigned long long)items, (unsigned long long)groups);
     }
+    {  // pairs, only the first intervals merged
+        uint64_t steps = 0, merged1 = 0;
+        for (int ty = 0; ty < tilesY; ++ty)
+            for (int tx = 0; tx < tilesX; tx += 2) {
+                auto& A = tiles[ty * tilesX + tx];
+                static std::vector<Iv> none;
+                auto& B = tx + 1 < tilesX ? tiles[ty * tilesX + tx + 1] : none;
+                size_t a = 0, b = 0;
+                if (!A.empty() && !B.empty() && A[0].key == B[0].key) {
+                    std::vector<uint32_t> q = A[0].cost;
+                    q.insert(q.end(), B[0].cost.begin(), B[0].cost.end());
+                    steps += makespan(q, false);
+                    a = b = 1;
+                    ++merged1;
+                }
+                for (; a < A.size(); ++a) steps += makespan(A[a].cost, false);
+                for (; b < B.size(); ++b) steps += makespan(B[b].cost, false);
+            }
+        std::printf("  pair-first %llu steps (util %.3f), %llu merged\n", (unsigned long long)steps,
+                    evalsTotal / (32.0 * steps), (unsigned long long)merged1);
+    }
     std::printf("%s: evals %llu  intervals %llu  ideal steps %llu\n", name.c_str(), (unsigned long long)evalsTotal,
                 (unsigned long long)ivs, (unsigned long long)((evalsTotal + 31) / 32));
     std::printf("  tile  %llu steps (util %.3f)\n", (unsigned long long)sTile, evalsTotal / (32.0 * sTile));
