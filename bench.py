@@ -464,12 +464,13 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     }
     traffic_path = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(traffic_path):  # dram read+write bytes of one k_march launch (ncu --set full, committed)
-        tr = json.load(open(traffic_path)).get("k_march")
-        if tr and args.config == "C3":
+        trs = json.load(open(traffic_path))
+        tr = trs.get(f"k_march@{args.config.lower()}")
+        if tr:
             result["roofline"]["traffic"] = tr["dram_bytes_per_launch"]
             result["roofline"]["traffic_source"] = tr["source"]
             if "fp32_executed_flops" in tr:
-                # the SASS FP32 work actually executed (2 FFMA + FADD + FMUL, ncu of one C3 launch) over the same
+                # the SASS FP32 work actually executed (2 FFMA + FADD + FMUL, ncu of one launch of this config) over the same
                 # live kernel time: appendix B credits the reference's formulas (e.g. 33 flop of quaternion
                 # transform that the fast path executes as 9 FFMA), the executed count does not
                 ex = tr["fp32_executed_flops"] / (march_ms * 1e-3) / 1e12

@@ -162,7 +162,10 @@ def main():
         import json as _json
         path = os.path.join(PROF, "latest_traffic.json")
         merged = _json.load(open(path)) if os.path.exists(path) else {}
+        # per (kernel, config tag) -- the bench reads the capture of its own
+        # config ("k_march@c3") -- and under the bare kernel name (latest)
         merged.update(traffic)
+        merged.update({f"{k}@{tag}": v for k, v in traffic.items()})
         open(path, "w").write(_json.dumps(merged, indent=1) + "\n")
     print("written to", PROF)
 
