@@ -50,7 +50,6 @@ struct FrameBufs {
     float4* tileFrustum = nullptr; // [tiles*4] inward unit normals of the pixel-centre pyramid
     float4* sbFrustum = nullptr;   // [superblocks*4] same for the superblock
     // A-buffer
-    uint2* pairs = nullptr;      // (voi, superblock)
     uint4* pool = nullptr;       // (tile, voi, entry bits, exit bits), unsorted
     uint4* unsorted = nullptr;   // CSR slots: (word, entry, exit, voi)
     Frag* frags = nullptr;       // CSR slots, sorted by (zEntry, word)
@@ -63,15 +62,12 @@ struct FrameBufs {
     uint32_t* counters = nullptr;    // see kCnt*
     // (volume, superblock) pairs grouped by superblock (k_tile's candidates)
     uint32_t* sbCount = nullptr;     // [superblocks] pairs per superblock
-    uint32_t* sbCursor = nullptr;    // [superblocks] scatter cursors
-    uint32_t* sbLocal = nullptr;     // [superblocks] exclusive scan inside a scan block
-    uint32_t* sbBlockSum = nullptr;
-    uint32_t* sbBlockPrefix = nullptr;
-    uint32_t* sbList = nullptr;      // [pairCap] volume indices, superblock-major
+    uint32_t* sbList = nullptr;      // [superblocks * sbCap] volume indices: superblock sb's candidates at sb * sbCap
     uint2* tileFrag = nullptr;       // [tiles] (first fragment, count) of each tile's sorted list in frags
     struct CullVol* cullVols = nullptr;  // [volumes] cull terms for the frame's camera (k_pairs -> k_tile_raster)
     RasterVol* rasterVols = nullptr; // [volumes] ray-test terms for the frame's camera (k_pairs -> k_tile_raster)
-    uint64_t pairCap = 0, poolCap = 0, fragCap = 0;
+    uint64_t poolCap = 0, fragCap = 0;
+    uint32_t sbCap = 0;              // candidates per superblock list (k_pairs fills them directly)
 };
 
 // device counters (uint32 slots)
@@ -84,8 +80,8 @@ enum : int {
     kCntOverflow = 5,
     kCntFallbackHard = 6,  // fast-path fallbacks without a usable view (full-tree gradient)
     kCntFrags = 7,         // fragments allocated (k_tile bump allocator)
-    kCntScanDone2 = 8,     // completion counter of the superblock scan
     kCntTileQueue = 9,     // k_tile work queue head
+    kCntSbNeed = 11,       // a superblock list overflowed: the capacity it needed (0: none)
     kCntSlots = 12
 };
 

@@ -129,12 +129,12 @@ struct bt_ctx {
     int width = 0, height = 0, tilesX = 0, tilesY = 0;
     DevBuf<float4> rays, cones, sbCones, tileFrustum, sbFrustum;
     DevBuf<float> coneSin;
-    DevBuf<uint2> pairs;
     DevBuf<uint4> pool, unsorted;
     DevBuf<Frag> frags;
     DevBuf<uint32_t> tileCount, tileCursor, tileLocal, blockSum, blockPrefix, offsets, counters;
     // (volume, superblock) pairs grouped by superblock, per-tile fragment lists
-    DevBuf<uint32_t> sbCount, sbCursor, sbLocal, sbBlockSum, sbBlockPrefix, sbList;
+    DevBuf<uint32_t> sbCount, sbList;
+    uint32_t sbCap = 0;  // candidates per superblock list
     DevBuf<uint2> tileFrag;
     bool haveAbuffer = false;
     bool haveRays = false;
@@ -244,7 +244,6 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.sbCones = c->sbCones.ptr;
     f.tileFrustum = c->tileFrustum.ptr;
     f.sbFrustum = c->sbFrustum.ptr;
-    f.pairs = c->pairs.ptr;
     f.pool = c->pool.ptr;
     f.unsorted = c->unsorted.ptr;
     f.frags = c->frags.ptr;
@@ -256,15 +255,11 @@ FrameBufs frame_bufs(const bt_ctx* c) {
     f.offsets = c->offsets.ptr;
     f.counters = c->counters.ptr;
     f.sbCount = c->sbCount.ptr;
-    f.sbCursor = c->sbCursor.ptr;
-    f.sbLocal = c->sbLocal.ptr;
-    f.sbBlockSum = c->sbBlockSum.ptr;
-    f.sbBlockPrefix = c->sbBlockPrefix.ptr;
     f.sbList = c->sbList.ptr;
+    f.sbCap = c->sbCap;
     f.rasterVols = c->rasterVols.ptr;
     f.cullVols = c->cullVols.ptr;
     f.tileFrag = c->tileFrag.ptr;
-    f.pairCap = std::min(c->pairs.cap, c->sbList.cap);
     f.poolCap = c->frags.cap;
     f.fragCap = std::min(c->frags.cap, c->unsorted.cap);
     return f;
@@ -374,12 +369,7 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     BT_CUDA(c->vCount.reserve(tiles));
     BT_CUDA(c->vBase.reserve(tiles));
     BT_CUDA(c->vCounters.reserve(4));
-    const size_t nsbscan = (nsb + kScanBlockElems - 1) / kScanBlockElems;
     BT_CUDA(c->sbCount.reserve(nsb));
-    BT_CUDA(c->sbCursor.reserve(nsb));
-    BT_CUDA(c->sbLocal.reserve(nsb));
-    BT_CUDA(c->sbBlockSum.reserve(nsbscan));
-    BT_CUDA(c->sbBlockPrefix.reserve(nsbscan + 1));
     BT_CUDA(c->tileFrag.reserve(tiles));
     BT_CUDA(c->tileCost.reserve(tiles));
     BT_CUDA(c->tileOrder.reserve(tiles * 2));
@@ -393,11 +383,15 @@ int ensure_image(bt_ctx* c, const bt_camera& cam) {
     return BT_OK;
 }
 
-int ensure_frame_caps(bt_ctx* c, size_t pairCap, size_t poolCap) {
+// sbCap: candidates per superblock list (k_pairs appends straight into them);
+// poolCap: fragments
+int ensure_frame_caps(bt_ctx* c, size_t sbCap, size_t poolCap) {
     bool moved = false;
-    if (pairCap > c->pairs.cap) {
-        BT_CUDA(c->pairs.reserve(pairCap));
-        BT_CUDA(c->sbList.reserve(pairCap));
+    const size_t nsb = superblock_count(c->tilesX, c->tilesY);
+    sbCap = std::max<size_t>(sbCap, c->sbCap);
+    if (sbCap > c->sbCap || nsb * sbCap > c->sbList.cap) {
+        BT_CUDA(c->sbList.reserve(nsb * sbCap));
+        c->sbCap = (uint32_t)sbCap;
         moved = true;
     }
     if (poolCap > c->frags.cap) {  // the fragment store (and its CSR / overflow staging)
@@ -504,8 +498,11 @@ int ensure_view_caps(bt_ctx* c) {
 // an overflow degrades to an empty, flagged A-buffer / record set.
 int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, bool checked,
                uint32_t mode = kTileRaster, const TraceParams* tp = nullptr) {
-    if (c->pairs.cap == 0) {
-        int rc = ensure_frame_caps(c, std::max<size_t>(1u << 18, (size_t)c->nvoi * 16), 1u << 20);
+    {  // first frame: a guess of the superblock lists' size (the checked path grows them); an image
+       // resize: the same capacity over the new superblock count
+        const size_t nsb = std::max<size_t>(1, superblock_count(c->tilesX, c->tilesY));
+        const size_t guess = c->sbCap ? c->sbCap : std::max<size_t>(256, 2 * (size_t)c->nvoi * 16 / nsb);
+        int rc = ensure_frame_caps(c, guess, c->frags.cap ? c->frags.cap : (size_t)1u << 20);
         if (rc) return rc;
     }
     if (mode & kTileViews) {
@@ -525,12 +522,12 @@ int do_abuffer(bt_ctx* c, const bt_camera& cam, uint32_t tile0, uint32_t tile1, 
         if (mode & kTileViews)
             BT_CUDA(cudaMemcpyAsync(vc, c->vCounters.ptr, sizeof(vc), cudaMemcpyDeviceToHost, c->stream));
         BT_CUDA(cudaStreamSynchronize(c->stream));
-        const bool pairOver = cnt[kCntPairs] > frame_bufs(c).pairCap;
+        const bool pairOver = cnt[kCntSbNeed] != 0u;  // a superblock list overflowed
         const bool fragOver = !pairOver && cnt[kCntFrags] > frame_bufs(c).fragCap;
         const bool ivOver = !pairOver && !fragOver && (mode & kTileViews) && (vc[2] > c->vIv.cap || vc[3] > c->vNodes.cap);
         if (!pairOver && !fragOver && !ivOver) break;
         // (lost pairs also lose their fragments and records: grow one thing at a time)
-        int rc = ensure_frame_caps(c, pairOver ? (size_t)cnt[kCntPairs] * 2 : c->pairs.cap,
+        int rc = ensure_frame_caps(c, pairOver ? (size_t)cnt[kCntSbNeed] * 3 / 2 + 64 : c->sbCap,
                                    fragOver ? (size_t)cnt[kCntFrags] * 2 : c->frags.cap);
         if (rc) return rc;
         if (ivOver) {
@@ -764,7 +761,6 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->tileFrustum.release();
     c->sbFrustum.release();
     c->coneSin.release();
-    c->pairs.release();
     c->pool.release();
     c->unsorted.release();
     c->frags.release();
@@ -775,7 +771,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     c->stats.release();
     c->gradScratch.release();
     for (auto* b : {&c->vCount, &c->vBase, &c->vNodes, &c->tileFrag}) b->release();
-    for (auto* b : {&c->sbCount, &c->sbCursor, &c->sbLocal, &c->sbBlockSum, &c->sbBlockPrefix, &c->sbList}) b->release();
+    for (auto* b : {&c->sbCount, &c->sbList}) b->release();
     c->vIv.release();
     c->vCounters.release();
     c->tileOrder.release();
@@ -1414,7 +1410,7 @@ int bt_abuffer_upload(bt_ctx* c, const bt_camera* cam, const uint32_t* offsets, 
     if (total && !frags) return fail(BT_EINVAL, "null fragments");
     for (uint32_t i = 0; i < tiles; ++i)
         if (offsets[i + 1] < offsets[i]) return fail(BT_EINVAL, "offsets must be non-decreasing");
-    rc = ensure_frame_caps(c, std::max<size_t>(c->pairs.cap, 1u << 16), std::max<size_t>(total, 1u << 16));
+    rc = ensure_frame_caps(c, std::max<uint32_t>(c->sbCap, 256u), std::max<size_t>(total, 1u << 16));
     if (rc) return rc;
     BT_CUDA(cudaMemcpyAsync(c->offsets.ptr, offsets, (tiles + 1) * 4, cudaMemcpyHostToDevice, c->stream));
     if (total)
@@ -1545,7 +1541,6 @@ int bt_render_frame(bt_ctx* c, const bt_camera* cam, const bt_render_config* cfg
             const size_t nsb = superblock_count(c->tilesX, c->tilesY);
             BT_CUDA(cudaMemsetAsync(c->counters.ptr, 0, kCntSlots * sizeof(uint32_t), c->side));
             BT_CUDA(cudaMemsetAsync(c->sbCount.ptr, 0, nsb * sizeof(uint32_t), c->side));
-            BT_CUDA(cudaMemsetAsync(c->sbCursor.ptr, 0, nsb * sizeof(uint32_t), c->side));
             BT_CUDA(cudaMemsetAsync(c->tileQueue.ptr, 0, sizeof(uint32_t), c->side));
             BT_CUDA(cudaEventRecord(c->evJoin[0], c->side));
             c->prezeroed = true;
@@ -1957,7 +1952,7 @@ int bt_stats_download(bt_ctx* c, bt_stats* out) {
     out->normalFallbacks = st[kStFallbacks];
     out->warpSteps = st[kStWarpSteps];
     if (c->haveAbuffer) out->fragments = cnt[kCntFrags];  // the per-tile lists' total (k_tile)
-    if (cnt[kCntOverflow] || cnt[kCntPairs] > frame_bufs(c).pairCap)
+    if (cnt[kCntOverflow] || cnt[kCntSbNeed])
         return fail(BT_ENOMEM, "A-buffer capacity overflowed during a graph replay; re-run eagerly");
     if (c->vCounters.ptr) {
         uint32_t vc[2] = {0u, 0u};

@@ -301,12 +301,11 @@ __global__ void __launch_bounds__(256) k_pairs(Cam cam, const Voi* vois, uint32_
         }
         const uint32_t m = __ballot_sync(kFull, pass);
         if (m == 0u) continue;
-        uint32_t slot = 0;
-        if (lane == 0) slot = atomicAdd(&fb.counters[kCntPairs], (uint32_t)__popc(m));
-        slot = __shfl_sync(kFull, slot, 0) + __popc(m & ((1u << lane) - 1u));
-        if (pass && slot < fb.pairCap) {
-            fb.pairs[slot] = make_uint2(warp, (uint32_t)sb);
-            atomicAdd(&fb.sbCount[sb], 1u);  // lanes of a warp hold distinct superblocks
+        if (lane == 0) atomicAdd(&fb.counters[kCntPairs], (uint32_t)__popc(m));
+        if (pass) {  // straight into the superblock's list (lanes of a warp hold distinct superblocks)
+            const uint32_t slot = atomicAdd(&fb.sbCount[sb], 1u);
+            if (slot < fb.sbCap) fb.sbList[(size_t)sb * fb.sbCap + slot] = warp;
+            else atomicMax(&fb.counters[kCntSbNeed], slot + 1u);  // the checked path grows sbCap
         }
     }
 }
@@ -382,21 +381,6 @@ __global__ void __launch_bounds__(1024) k_scan(ScanArgs a, uint32_t n) {
             a.blockPrefix[gridDim.x] = carry;
             *a.done = 0u;  // ready for the next scan on this counter
         }
-    }
-}
-
-__device__ __forceinline__ uint32_t sb_offset(const FrameBufs& fb, uint32_t sb) {
-    return fb.sbLocal[sb] + fb.sbBlockPrefix[sb / kScanBlock];
-}
-
-// (volume, superblock) pairs -> per-superblock candidate lists (list order is
-// free: a tile's fragments are sorted by (zEntry, word, volume) afterwards)
-__global__ void k_sb_scatter(FrameBufs fb) {
-    if ((uint64_t)fb.counters[kCntPairs] > fb.pairCap) return;  // overflow: k_tile flags the frame
-    const uint32_t n = fb.counters[kCntPairs];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint2 pr = fb.pairs[i];
-        fb.sbList[sb_offset(fb, pr.y) + atomicAdd(&fb.sbCursor[pr.y], 1u)] = pr.x;
     }
 }
 
@@ -493,7 +477,6 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
     if (zero) {
         cudaMemsetAsync(fb.counters, 0, kCntSlots * sizeof(uint32_t), st);
         cudaMemsetAsync(fb.sbCount, 0, nsbAll * sizeof(uint32_t), st);
-        cudaMemsetAsync(fb.sbCursor, 0, nsbAll * sizeof(uint32_t), st);
     }
     if (nvoi > 0) {
         int sbLo, sbHi;
@@ -507,9 +490,6 @@ void launch_abuffer(cudaStream_t st, const Cam& cam, const Voi* vois, uint32_t n
         const dim3 grid((nvoi * 32 + 255) / 256, chunks);
         k_pairs<<<grid, 256, 0, st>>>(cam, vois, nvoi, fb, tilesX, tilesY, tile0, tile1, sbLo, sbHi);
     }
-    ScanArgs a{fb.sbCount, fb.sbLocal, fb.sbBlockSum, fb.sbBlockPrefix, fb.counters + kCntScanDone2};
-    k_scan<<<(nsbAll + kScanBlock - 1) / kScanBlock, 1024, 0, st>>>(a, nsbAll);
-    if (nvoi > 0) k_sb_scatter<<<smCount * 2, 256, 0, st>>>(fb);
 }
 
 void launch_frag_csr(cudaStream_t st, const FrameBufs& fb, uint32_t tiles, int smCount) {

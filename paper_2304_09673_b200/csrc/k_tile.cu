@@ -123,7 +123,7 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
     }
     const int sbX = (tilesX + kSB - 1) / kSB;
     const uint32_t sb = (uint32_t)((ty / kSB) * sbX + tx / kSB);
-    const uint32_t nCand = fb.sbCount[sb];
+    const uint32_t nCand = min(fb.sbCount[sb], fb.sbCap);
     uint32_t nf = 0;
     tested = 0;
     for (uint32_t base = 0; base < nCand;) {
@@ -139,7 +139,7 @@ __device__ uint32_t raster_tile(const Cam& cam, const Voi* vois, const FrameBufs
         cone.cosH = c4.w;
         cone.sinH = fb.coneSin[tile];
         const float4* pyramid = fb.tileFrustum + (size_t)tile * 4;
-        const uint32_t* cand = fb.sbList + fb.sbLocal[sb] + fb.sbBlockPrefix[sb / kScanBlockElems];
+        const uint32_t* cand = fb.sbList + (size_t)sb * fb.sbCap;
         while (base < nCand && cnt + 32u <= kCullList) {
             const uint32_t j = base + lane;
             uint32_t vi = 0;
@@ -485,9 +485,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, BT_TILE_MINB)
     __shared__ RasterVol vstaged[kTileWarps][32];
     __shared__ float4 tileRays[kTileWarps][64];
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    // a (volume, superblock) pair list that outgrew its buffer: empty,
+    // a superblock candidate list that outgrew its capacity: empty,
     // flagged A-buffer (the checked path grows the buffers and rebuilds)
-    const bool pairsLost = (uint64_t)fb.counters[kCntPairs] > fb.pairCap;
+    const bool pairsLost = fb.counters[kCntSbNeed] != 0u;
     uint32_t testedSum = 0;
     for (uint32_t tile = next_tile(&fb.counters[kCntTileQueue], tile0); tile < tile1;
          tile = next_tile(&fb.counters[kCntTileQueue], tile0)) {
