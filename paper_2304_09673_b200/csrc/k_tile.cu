@@ -542,10 +542,12 @@ void launch_tile_pass(cudaStream_t st, uint32_t mode, const Cam& cam, const Trac
     const uint32_t tiles = (uint32_t)(tilesX * tilesY);
     cudaMemsetAsync(fb.counters + kCntTileQueue, 0, 2 * sizeof(uint32_t), st);
     // tiles outside [tile0, tile1) keep empty lists / no records (a sharded
-    // frame's normals read every tile's records)
-    if (mode & kTileRaster) cudaMemsetAsync(fb.tileFrag, 0, (size_t)tiles * sizeof(uint2), st);
+    // frame's normals read every tile's records); the passes write every
+    // tile of their range, so a whole frame needs no clearing
+    const bool partial = tile0 != 0u || tile1 < tiles;
+    if ((mode & kTileRaster) && partial) cudaMemsetAsync(fb.tileFrag, 0, (size_t)tiles * sizeof(uint2), st);
     if (mode & kTileViews) {
-        cudaMemsetAsync(vb.count, 0, (size_t)tiles * sizeof(uint2), st);
+        if (partial) cudaMemsetAsync(vb.count, 0, (size_t)tiles * sizeof(uint2), st);
         cudaMemsetAsync(vb.counters, 0, 4 * sizeof(uint32_t), st);
     }
     if (tile1 <= tile0) return;
