@@ -401,3 +401,49 @@ def test_device_fast_indices_equal_host(rd, name):
     b = rd.download_gbuffer()
     for plane in ("hit", "depth", "evalCount", "tileMaxOverlap", "tileCacheBytes", "tileError"):
         assert getattr(a, plane).tobytes() == getattr(b, plane).tobytes(), plane
+
+
+def test_graph_replay_capacity_overflow_is_flagged_then_eager_frame_grows():
+    """A graph is captured on a frame whose buffers fit (tiny primitives), then
+    the parameters grow every primitive back (C4: 10,000 primitives at 4K) and
+    the graph is replayed: the fragment store and the superblock candidate
+    lists overflow.  The replay must stay in bounds and be flagged
+    (bt_stats_download -> BT_ENOMEM), and the next eager frame must grow the
+    buffers and render the frame bit-identically to a fresh context."""
+    from paper_2304_09673_b200._capi import BtError
+    cfg = RenderConfig()
+    s = Scene.build("C4")
+    w, p, c = s.perturb(1)
+    small = p.copy()
+    for i in range(len(c)):
+        small[i, 7:c[i]] *= 0.02  # shape parameters (radii, extents) -- the transforms stay
+    cam = s.device_camera
+    rd = Renderer(0)
+    fresh = Renderer(0)
+    try:
+        rd.upload(s)
+        rd.update_params(w, small, c)
+        rd.render_frame(cam, cfg, exact=False, graph=True)  # eager sizing on the small frame, then capture
+        rd.stats()
+        rd.update_params(w, p, c)
+        rd.reset_stats()
+        rd.render_frame(cam, cfg, exact=False, graph=True)  # replay of the small frame's graph
+        with pytest.raises(BtError):
+            rd.stats()
+        rd.reset_stats()
+        rd.render_frame(cam, cfg, exact=True, graph=False)  # checked: grows and renders
+        g = rd.download_gbuffer()
+        st = rd.stats()
+        assert st.tileErrors == 0 and g.hit.any()
+        fresh.upload(s)  # the scene's tree carries frame 1's parameters
+        fresh.render_frame(cam, cfg, exact=True, graph=False)
+        gf = fresh.download_gbuffer()
+        for plane in ("hit", "depth", "evalCount", "normal", "tileMaxOverlap", "tileCacheBytes", "tileError"):
+            assert getattr(g, plane).tobytes() == getattr(gf, plane).tobytes(), plane
+        # and the graph path recovers: the next captured frame equals the eager one
+        rd.render_frame(cam, cfg, exact=True, graph=True)
+        assert rd.download_gbuffer().depth.tobytes() == gf.depth.tobytes()
+        rd.stats()
+    finally:
+        rd.close()
+        fresh.close()
