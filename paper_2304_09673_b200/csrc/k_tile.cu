@@ -98,8 +98,8 @@ __device__ __forceinline__ bool raster_volume(const Cam& cam, const RasterVol& r
         entry = tmin2<Fm>(entry, __shfl_xor_sync(kFull, entry, o));
         exitv = tmax2<Fm>(exitv, __shfl_xor_sync(kFull, exitv, o));
     }
-    entryOut = ndc_from_view_z(cam, entry);
-    exitOut = ndc_from_view_z(cam, exitv);
+    entryOut = ndc_from_view_z_uniform(cam, entry);
+    exitOut = ndc_from_view_z_uniform(cam, exitv);
     return true;
 }
 
