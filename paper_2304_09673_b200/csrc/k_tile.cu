@@ -469,7 +469,7 @@ __device__ void views_tile_small(const Cam& cam, const TraceParams& tp, const Fr
 #define BT_RASTER_FM 1
 #endif
 #ifndef BT_TILE_MINB
-#define BT_TILE_MINB 6  // CTAs per SM the register budget of k_tile_raster must fit
+#define BT_TILE_MINB 7  // CTAs per SM the register budget of k_tile_raster must fit (62 registers)
 #endif
 __device__ __forceinline__ uint32_t next_tile(uint32_t* queue, uint32_t tile0) {
     uint32_t q = 0;
